@@ -1,0 +1,371 @@
+#!/usr/bin/env python
+"""Benchmark of the D2Q37 hot path (BASELINE.json metric) — prints ONE JSON line.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config weak1920|strong8192|weak4096] [--mode fused|split]
+
+A "step" is one full D2Q37 time step (pbc -> propagate -> bc -> collide, fused
+pull kernel) over the whole lattice.  N = 1: config #2 of BASELINE.json, the
+1920x2048 lattice; N > 1 (torchrun, one rank per GPU, NCCL ring exchange):
+weak scaling with 1920x2048 per GPU (global lattice 1920N x 2048).  value =
+lattice sites of all ranks x K / max-over-ranks device time (MLUPS).
+
+Extra keys: roofline (dominant kernel k_step_fused vs the
+measured HBM copy bandwidth), kernels (split-mode propagate / bc / collide per
+kernel, collide FP64 % of the measured peak), e2e (same metric through the C
+ABI with pinned host buffers: state upload, per-step invariants read-back,
+final gather), clocks (NVML samples during the timed region), cpu_baseline
+(the CPU oracle on a bounded sample of the same workload, rank 0 at N=1).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "D2Q37 fp64 MLUPS at 1/2/4/8 B200; propagate HBM GB/s, collide FP64 % of peak"
+BYTES_PER_SITE = 592  # 37 fp64 reads + 37 fp64 writes (Table 1 convention)
+CONFIGS = {
+    # name: (lx per GPU or global, ly, scaling)
+    "weak1920": (1920, 2048, "weak"),     # BASELINE configs[1] per GPU
+    "weak4096": (4096, 8192, "weak"),     # BASELINE configs[3]
+    "strong8192": (8192, 8192, "strong"), # BASELINE configs[2]
+}
+
+
+def load_json(path, default=None):
+    try:
+        with open(path) as fh:
+            return json.load(fh)
+    except Exception:
+        return default
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons while the timed region runs."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int, period: float = 0.005):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.period = period
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t is not None:
+            self._t.join()
+            # one sample after the region too, in case it was shorter than the period
+            if not self.samples:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+
+    def summary(self):
+        if self.nv is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml_unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- oracle leg
+
+def oracle_throughput(lx_total: int, ly: int, budget_s: float, steps: int | None = None):
+    """The CPU oracle, as it stands, on a bounded sample of the workload: the
+    first w columns of the same RT lattice (all ly rows), w sized so the run
+    takes about budget_s.  Returns (MLUPS, cores, sample description)."""
+    import lbgen
+    import oracle
+    T0 = oracle.t0()
+    probe_w = min(lx_total, 16)
+    o = oracle.Lattice(probe_w, ly)
+    o.init_macro(*lbgen.rt_macro(lx_total, ly, T0, lx=probe_w))
+    t = time.perf_counter()
+    o.step(1)
+    per_site = (time.perf_counter() - t) / (probe_w * ly)
+    nsteps = steps if steps is not None else 3
+    w = int(max(3, min(lx_total, budget_s / (per_site * ly * nsteps))))
+    o = oracle.Lattice(w, ly)
+    o.init_macro(*lbgen.rt_macro(lx_total, ly, T0, lx=w))
+    t = time.perf_counter()
+    o.step(nsteps)
+    dt = time.perf_counter() - t
+    mlups = w * ly * nsteps / dt / 1e6
+    sample = (f"oracle lbref (C, -O2 -ffp-contract=off, OpenMP over ix) full steps on columns 0..{w - 1} "
+              f"of the {lx_total}x{ly} RT workload, {nsteps} steps, {dt:.1f} s")
+    return mlups, oracle.threads(), sample, dt, w, nsteps
+
+
+def run_reference(args, cfg_name, lx_total, ly, scaling, rank, world):
+    if rank != 0:
+        return
+    budget = float(os.environ.get("LB_REF_BUDGET_S", "60"))
+    per_step = budget / max(1, args.steps + args.warmup)
+    import oracle
+    import lbgen
+    T0 = oracle.t0()
+    probe_w = min(lx_total, 16)
+    o = oracle.Lattice(probe_w, ly)
+    o.init_macro(*lbgen.rt_macro(lx_total, ly, T0, lx=probe_w))
+    t = time.perf_counter()
+    o.step(1)
+    per_site = (time.perf_counter() - t) / (probe_w * ly)
+    w = int(max(3, min(lx_total, per_step / (per_site * ly))))
+    o = oracle.Lattice(w, ly)
+    o.init_macro(*lbgen.rt_macro(lx_total, ly, T0, lx=w))
+    o.step(args.warmup)
+    t = time.perf_counter()
+    o.step(args.steps)
+    dt = time.perf_counter() - t
+    value = w * ly * args.steps / dt / 1e6
+    sample = (f"each step = one full oracle step on columns 0..{w - 1} (all {ly} rows) of the "
+              f"{lx_total}x{ly} RT workload")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "MLUPS", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": workload_config(cfg_name, lx_total, ly, world, args.mode),
+        "cpu_baseline": {"value": value, "unit": "MLUPS", "cores": oracle.threads(), "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "MLUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(cfg_name, lx_total, ly, world, mode):
+    return {"workload": f"D2Q37 fp64 {lx_total}x{ly} lattice, periodic X + thermal walls Y, "
+                        f"Rayleigh-Taylor init, {mode} step" + (f", X-slab on {world} GPUs" if world > 1 else ""),
+            "name": cfg_name, "lx_total": lx_total, "ly": ly, "sites": lx_total * ly, "mode": mode,
+            "parallelism": f"xslab{world}", "l2": "inputs exceed L2 (2 x 1.19 GB/GPU vs 126 MB), no flush",
+            "tau": 0.8, "bc_y": "thermal", "init": "isobaric RT (lbgen, seed 1703)"}
+
+
+# ----------------------------------------------------------------------------- our leg
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="weak1920", choices=sorted(CONFIGS))
+    ap.add_argument("--mode", default="fused", choices=["fused", "split"])
+    ap.add_argument("--overlap", type=int, default=-1, help="-1: auto (on for N>1)")
+    ap.add_argument("--no-extras", action="store_true", help="skip e2e / split pass / cpu baseline")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    lx_cfg, ly, scaling = CONFIGS[args.config]
+    lx_total = lx_cfg * world if scaling == "weak" else lx_cfg
+
+    if args.impl == "reference":
+        run_reference(args, args.config, lx_total, ly, scaling, rank, world)
+        return
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import lbgen
+    import paper_1703_00186_b200 as lb
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        obj = [lb.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    else:
+        nccl_id = None
+    overlap = (world > 1) if args.overlap < 0 else bool(args.overlap)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    T0 = lb.t0()
+    g = lb.Lattice(lx_total, ly, mode=args.mode, overlap=overlap, rank=rank, nranks=world, nccl_id=nccl_id)
+    lx = g.lx
+    fields = lbgen.rt_macro(lx_total, ly, T0, x0=rank * lx, lx=lx)
+    g.init_macro(*fields)
+    stream = torch.cuda.current_stream()
+
+    # ---- warm-up, then exactly K timed steps (device time, max over ranks)
+    g.step(args.warmup)
+    g.sync()
+    g.profile(True)
+    g.profile_reset()
+    launches0 = g.launch_count()
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        e0.record(stream)
+        g.step(args.steps)
+        e1.record(stream)
+        g.sync()
+        torch.cuda.synchronize()
+    barrier()
+    launches = g.launch_count() - launches0
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    prof = g.profile_read()
+    g.profile(False)
+    sites_all = lx_total * ly
+    value = sites_all * args.steps / (ms * 1e-3) / 1e6
+
+    peaks = load_json(os.path.join(ROOT, "MEASURED_PEAKS.json"), {}) or {}
+    hbm_peak = peaks.get("hbm_gbs")
+    peak_src = "MEASURED_PEAKS.json hbm_gbs (driver-measured copy)"
+    if not hbm_peak:
+        hbm_peak, peak_src = 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+    ncu = load_json(os.path.join(ROOT, "profiles", "ncu_summary.json"), {}) or {}
+    fp64 = load_json(os.path.join(ROOT, "profiles", "r01_fp64_hbm_microbench.json"), {}) or {}
+    fp64_peak = fp64.get("fp64_tflops")
+
+    fk = prof.get("k_step_fused") or prof.get("k_propagate")
+    kname = "k_step_fused" if "k_step_fused" in prof else "k_propagate"
+    roofline = None
+    if fk and fk["launches"]:
+        avg_ms = fk["total_ms"] / fk["launches"]
+        bytes_per_launch = BYTES_PER_SITE * fk["units"] / fk["launches"]
+        achieved = bytes_per_launch / (avg_ms * 1e-3) / 1e9
+        kn = ncu.get("kernels", {}).get(kname, {})
+        traffic = kn.get("dram_bytes_per_site")
+        roofline = {"kernel": kname, "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak,
+                    "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
+                    "traffic": (traffic * fk["units"] / fk["launches"]) if traffic else None,
+                    "algorithmic_bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_ms,
+                    "share_of_step": fk["total_ms"] / ms if world == 1 else None,
+                    "peak_source": peak_src,
+                    "traffic_source": ncu.get("source") if traffic else None}
+
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "MLUPS", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": workload_config(args.config, lx_total, ly, world, args.mode),
+        "clocks": clk.summary(), "gpu_launches": int(launches),
+        "roofline": roofline,
+        "kernel_times_ms": {k: {"avg_ms": v["total_ms"] / max(1, v["launches"]), "launches": v["launches"]}
+                            for k, v in prof.items()},
+    }
+    line["config"]["overlap"] = overlap
+
+    if not args.no_extras:
+        # ---- per-kernel split pass (propagate GB/s, collide FP64 % of peak)
+        gs = lb.Lattice(lx_total, ly, mode="split", rank=rank, nranks=world, nccl_id=None) if world == 1 else None
+        if gs is not None:
+            del g
+            torch.cuda.empty_cache()
+            gs.init_macro(*fields)
+            gs.step(3)
+            gs.profile(True)
+            gs.profile_reset()
+            gs.step(10)
+            sp = gs.profile_read()
+            kern = {}
+            for k, v in sp.items():
+                avg = v["total_ms"] / max(1, v["launches"])
+                kern[k] = {"avg_ms": avg, "launches": v["launches"]}
+                if k in ("k_propagate", "k_collide"):
+                    per = BYTES_PER_SITE * v["units"] / v["launches"]
+                    kern[k]["gbs"] = per / (avg * 1e-3) / 1e9
+                    kern[k]["hbm_frac"] = kern[k]["gbs"] / hbm_peak
+                if k == "k_collide":
+                    kern[k]["mlups"] = v["units"] / v["launches"] / (avg * 1e-3) / 1e6
+                    fl = ncu.get("kernels", {}).get("k_collide", {}).get("flops_per_site")
+                    if fl and fp64_peak:
+                        tf = fl * kern[k]["mlups"] * 1e6 / 1e12
+                        kern[k].update({"flops_per_site_ncu": fl, "fp64_tflops": tf,
+                                        "fp64_frac": tf / fp64_peak, "fp64_peak_tflops": fp64_peak})
+                    kern[k]["paper_convention_6500_flop_tflops"] = 6500 * kern[k]["mlups"] * 1e6 / 1e12
+            split_ms = sum(v["total_ms"] for v in sp.values()) / 10
+            kern["split_step_mlups"] = lx_total * ly / (split_ms * 1e-3) / 1e6
+            line["kernels"] = kern
+            g = gs
+        # ---- e2e through the C ABI with pinned host buffers
+        state_bytes = 37 * g.sites * 8
+        host_in = torch.empty(37 * g.sites, dtype=torch.float64).pin_memory()
+        host_out = torch.empty((37, lx_total, ly), dtype=torch.float64).pin_memory() if rank == 0 else None
+        st0 = g.gather() if world == 1 else None
+        if st0 is not None:
+            host_in.numpy()[:] = st0.reshape(-1)
+        k_e2e = max(10, min(args.steps, 100))
+        barrier()
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        g.set_state(host_in.numpy())
+        for _ in range(k_e2e):
+            g.step(1)
+            g.invariants()
+        out = g.gather(out=host_out.numpy() if host_out is not None else None)
+        e2e_s = max_over_ranks(time.perf_counter() - t)
+        line["e2e"] = {"value": round(sites_all * k_e2e / e2e_s / 1e6, 2), "unit": "MLUPS",
+                       "h2d_bytes_per_step": state_bytes / k_e2e,
+                       "d2h_bytes_per_step": (state_bytes + 5 * 8 * k_e2e) / k_e2e,
+                       "steps": k_e2e,
+                       "timed": "lb_set_state(pinned host) + K x (lb_step(1) + lb_invariants -> host) + lb_gather(pinned host)"}
+        del out
+        # ---- CPU oracle baseline (rank 0, N = 1 only)
+        if world == 1 and rank == 0:
+            mlups, cores, sample, dt, w, ns = oracle_throughput(lx_total, ly,
+                                                                float(os.environ.get("LB_CPU_BUDGET_S", "15")))
+            line["cpu_baseline"] = {"value": round(mlups, 3), "unit": "MLUPS", "cores": cores,
+                                    "kind": "oracle", "sample": sample}
+
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,224 @@
+/*
+ * lb.h — C ABI of the B200-native D2Q37 thermal Lattice Boltzmann hot path
+ * (arXiv 1703.00186, Calore et al., CCPE 28:3485).  Library: liblb_d2q37.so
+ * (paper_1703_00186_b200/), hand-written sm_100a CUDA kernels.
+ *
+ * Citations "P:a-b" are lines of the paper text; "G<n>" are the
+ * readings of the paper listed in DESIGN.md §3; "§8x" are rows of SURVEY.md §8.
+ *
+ * ---------------------------------------------------------------------------
+ * What one time step computes (Eq. 1 at P:183-187):
+ *   pbc       periodic-X halo columns (3 per side, all 37 populations)   §8a1
+ *   propagate B[l, x] = A[l, x - c_l]  (pull; populations hop <= 3 sites) §8a2
+ *   bc        top/bottom walls: specular mirror + thermal repopulation   §8a3
+ *   collide   f <- f - (dt/tau)(f - f_eq(rho, u, T)), moments of Eq. 2   §8a4
+ *   swap      A <-> B                                                    §8a7
+ * fused mode does propagate+bc+collide in one pull pass A -> B (§8a5) and is
+ * bit-identical to split mode.  With N ranks the lattice is split into X
+ * slabs on a ring; the halo exchange runs on a communication
+ * stream overlapped with the bulk columns (§8a6).
+ *
+ * ---------------------------------------------------------------------------
+ * Layouts.
+ *   canonical (host side of lb_set_state / lb_gather / lb_init_macro):
+ *     populations  [37][Lx][Ly]  doubles, iy fastest, physical sites only
+ *                  (the SoA order of P:493-496 with halos stripped);
+ *     macro fields [Lx][Ly]      doubles.
+ *     Population labels follow G2: l = 0..36 enumerates c = (cx, cy) with cx
+ *     from +3 down to -3 and cy ascending; l = 0 is (3,-1), l = 1 is (3,0)
+ *     (P:452-453), l = 18 is the rest population.
+ *   internal (device buffers f_a, f_b; "column-blocked SoA"):
+ *     element (ix, l, r) at  (ix * 37 + l) * nyp + r,
+ *     ix in [0, Lx+6): columns, physical columns are [3, 3+Lx);
+ *     r in [0, nyp): rows, physical row y (0-based) is r = y0 + y, the
+ *     y-halo rows are [y0-3, y0) and [y0+Ly, y0+Ly+3).  y0 and nyp are
+ *     multiples of 16 doubles (128 B), so every physical column starts on a
+ *     128-byte boundary.  Each column holds the 37 population rows of one
+ *     lattice column contiguously, so a rank's 3 halo / border columns are one
+ *     contiguous block of 3*37*nyp doubles (no packing for the exchange).
+ *
+ * Ownership.  The caller allocates f_a and f_b (lb_layout.elems doubles each,
+ * 16-byte aligned device memory, e.g. torch tensors) and keeps them alive
+ * until lb_destroy returns; the library borrows them.  The context owns its
+ * streams, events, NCCL communicator and small scratch; lb_destroy frees them.
+ *
+ * Errors.  Every call returns an int status (LB_OK = 0).  No exception crosses
+ * the ABI.  Calls other than lb_gather, lb_invariants, lb_sync and
+ * lb_profile_read only enqueue work on the context's stream; an error of an
+ * asynchronous kernel surfaces at the next synchronising call as LB_ECUDA.
+ * lb_last_error() gives a human-readable message for the calling thread.
+ *
+ * Threading.  One context per process and GPU; a context is not thread-safe.
+ */
+#ifndef LB_D2Q37_H
+#define LB_D2Q37_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LB_Q 37    /* populations per site                      */
+#define LB_HALO 3  /* halo width Hx = Hy = 3        */
+
+/* status codes (SPEC S:469 exit-code classes: rejected = 2, blow-up = 3) */
+enum lb_status {
+  LB_OK = 0,
+  LB_EINVAL = 1,     /* invalid argument or parameter set                   */
+  LB_ESTATE = 2,     /* call out of order (e.g. lb_gather mid-step)         */
+  LB_ECUDA = 3,      /* CUDA runtime / kernel error                          */
+  LB_ENCCL = 4,      /* NCCL error                                           */
+  LB_ENONPHYS = 5,   /* NaN or rho <= 0 detected by lb_invariants            */
+  LB_ENOMEM = 6      /* host or device allocation failed                     */
+};
+
+enum lb_bc_y {
+  LB_WALL_THERMAL = 0,   /* mirror + thermal repopulation at T_bottom/T_top (G9) */
+  LB_WALL_ADIABATIC = 1, /* mirror only                                          */
+  LB_PERIODIC = 2        /* no bc; y-halo rows wrapped by pbc (test geometry)    */
+};
+
+enum lb_mode {
+  LB_MODE_FUSED = 0,     /* one pull kernel: propagate+bc+collide, A -> B     */
+  LB_MODE_SPLIT = 1      /* propagate, bc, collide as separate kernels        */
+};
+
+typedef struct lb_params {
+  int lx_total;          /* global physical columns (X, decomposed)           */
+  int ly;                /* physical rows (Y, never decomposed)               */
+  double tau;            /* relaxation time (Eq. 1)                           */
+  double dt;             /* time step (Eq. 1); 0 < dt/tau <= 2                */
+  double t_bottom;       /* wall temperature at y = -1/2  (lattice units)     */
+  double t_top;          /* wall temperature at y = Ly - 1/2                  */
+  int bc_y;              /* enum lb_bc_y                                       */
+  int mode;              /* enum lb_mode                                       */
+  int overlap;           /* 1: exchange || bulk, then borders     */
+} lb_params;
+
+typedef struct lb_dist {
+  int rank;              /* this process' slab, 0..nranks-1                    */
+  int nranks;            /* ring size N; lx_total % N == 0                     */
+  const unsigned char* nccl_id; /* 128-byte ncclUniqueId from rank 0, or NULL if N == 1 */
+} lb_dist;
+
+typedef struct lb_layout {
+  int lx;                /* physical columns of this rank = lx_total / N       */
+  int ly;                /* physical rows                                      */
+  int nx;                /* lx + 6 columns (3 halo columns per side)          */
+  int nyp;               /* padded rows per population column (mult. of 16)   */
+  int y0;                /* internal row of physical row 0 (multiple of 16)   */
+  int x0_global;         /* global index of this rank's first physical column */
+  int64_t col_stride;    /* 37 * nyp doubles between consecutive columns       */
+  int64_t elems;         /* doubles per buffer = nx * col_stride               */
+  int64_t bytes;         /* elems * 8                                          */
+  int64_t sites;         /* lx * ly physical sites of this rank                */
+} lb_layout;
+
+typedef struct lb_ctx lb_ctx;
+
+/* Per-kernel timing record (see lb_profile_enable). */
+typedef struct lb_kprof {
+  char name[32];         /* kernel name, e.g. "k_step_fused"                   */
+  int64_t launches;      /* launches timed since the last reset               */
+  double total_ms;       /* summed CUDA-event time of those launches          */
+  int64_t units;         /* lattice sites those launches processed            */
+} lb_kprof;
+
+/* ---- host-only queries (no GPU needed) ---------------------------------- */
+
+/* Validate p for (rank, nranks) and fill *out.  Rules: lx_total % nranks == 0;
+ * per-rank lx >= 3 (N = 1) or >= 6 (N > 1, so the 3+3 border columns are
+ * disjoint); ly >= 6 for walls (>= 3 periodic); 0 < dt/tau <= 2; wall
+ * temperatures > 0; enums in range.  Returns LB_EINVAL otherwise. */
+int lb_query_layout(const lb_params* p, int rank, int nranks, lb_layout* out);
+
+/* The D2Q37 constants the library uses (host copies; DESIGN.md App. A):
+ * c[37][2] lattice velocities (label order G2), w[37] weights, *a the scale
+ * factor, *t0 = 1/a^2 the reference temperature (G3).  Any pointer may be NULL. */
+int lb_constants(int* c, double* w, double* a, double* t0);
+
+/* Wall constants K_wall,l(T_wall) (App. B, canonical expression tree G16)
+ * exactly as uploaded by lb_init: K[37]. */
+int lb_kwall(double t_wall, double* K);
+
+/* ncclGetUniqueId into out[128] (rank 0 calls it; broadcast it to the others). */
+int lb_nccl_unique_id(unsigned char* out);
+
+/* Message for the last failing call on this thread (static storage). */
+const char* lb_last_error(void);
+const char* lb_strerror(int status);
+
+/* ---- context ------------------------------------------------------------ */
+
+/* Create a context on the current CUDA device.  f_a, f_b: caller-owned
+ * device buffers of lb_layout.elems doubles (16-byte aligned).  stream: the
+ * cudaStream_t all compute work is enqueued on (NULL = legacy default
+ * stream).  Zero-fills both buffers (so halo rows are deterministic, G10),
+ * uploads K_wall for t_bottom / t_top, and for nranks > 1 creates the NCCL
+ * communicator from d->nccl_id plus a high-priority communication stream.
+ * Synchronising. */
+int lb_init(const lb_params* p, const lb_dist* d, double* f_a, double* f_b,
+            void* stream, lb_ctx** out);
+void lb_destroy(lb_ctx* ctx);
+int lb_get_layout(const lb_ctx* ctx, lb_layout* out);
+int lb_set_stream(lb_ctx* ctx, void* stream);
+
+/* A := f_eq(rho, u, T) (App. B) on this rank's physical sites.  rho, ux, uy,
+ * T: [Lx][Ly] doubles (this rank's columns), in host memory if on_device == 0
+ * (pageable or pinned), else device memory.  Uses B as staging and re-zeroes
+ * it.  Only at a step boundary (LB_ESTATE otherwise). */
+int lb_init_macro(lb_ctx* ctx, const double* rho, const double* ux,
+                  const double* uy, const double* T, int on_device);
+
+/* A := populations given in canonical local layout [37][Lx][Ly] (host memory
+ * if on_device == 0, else device).  Only at a step boundary. */
+int lb_set_state(lb_ctx* ctx, const double* canon, int on_device);
+
+/* ---- the hot path (§8b): each call enqueues on the context stream ------- */
+
+int lb_exchange(lb_ctx* ctx);   /* pbc on A (§8a1): wrap (N=1) or NCCL ring   */
+int lb_propagate(lb_ctx* ctx);  /* raw pull A -> B (§8a2); entries pulled from
+                                   the y-halo stay zero until lb_bc            */
+int lb_bc(lb_ctx* ctx);         /* walls on B reading A (§8a3); no-op if PERIODIC */
+int lb_collide(lb_ctx* ctx);    /* in place on B (§8a4), THEN swaps A <-> B, so
+                                   exchange, propagate, bc, collide == lb_step(1) */
+int lb_step(lb_ctx* ctx, int nsteps); /* nsteps full steps in p->mode, with the
+                                   overlapped schedule when p->overlap         */
+
+/* ---- results ------------------------------------------------------------ */
+
+/* Collective over the ring.  Physical state A in canonical GLOBAL layout
+ * [37][lx_total][Ly] written to host_out on rank `root` (other ranks may pass
+ * NULL).  Uses B as device staging; only at a step boundary.  Synchronising. */
+int lb_gather(lb_ctx* ctx, double* host_out, int root);
+
+/* Debug view: this rank's physical sites of buffer which (0 = A, 1 = B) in
+ * canonical local layout [37][Lx][Ly], converted on the host; allowed mid-step
+ * (e.g. between lb_propagate and lb_bc).  Synchronising. */
+int lb_peek(lb_ctx* ctx, int which, double* host_out);
+
+/* Collective.  out[0..3] = global sum over physical sites of rho, j_x, j_y
+ * and E = 1/2 sum_l |c_l|^2 f_l, out[4] = global minimum site density.
+ * Deterministic for a fixed N (fixed-order block partials).  Returns
+ * LB_ENONPHYS if any value is NaN or min rho <= 0.  Synchronising. */
+int lb_invariants(lb_ctx* ctx, double* out);
+
+int lb_sync(lb_ctx* ctx);
+
+/* ---- instrumentation ----------------------------------------------------- */
+
+/* enable != 0: bracket every kernel launch with CUDA events on the stream it
+ * is launched on and accumulate per-kernel time (lb_profile_read, which
+ * synchronises).  Costs two event records per launch.  Disabled by default. */
+int lb_profile_enable(lb_ctx* ctx, int enable);
+int lb_profile_reset(lb_ctx* ctx);
+/* Fills up to max records; *n receives the number of distinct kernels. */
+int lb_profile_read(lb_ctx* ctx, lb_kprof* out, int max, int* n);
+/* Number of kernel launches the library issued since lb_init (all streams). */
+int64_t lb_launch_count(const lb_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LB_D2Q37_H */

@@ -1,0 +1,622 @@
+// lb_api.cu — the C ABI of include/lb.h: context, validation, the step
+// scheduler (split / fused, bulk || exchange then borders), NCCL ring
+// exchange, state I/O, invariants and per-kernel instrumentation.
+#include "../../include/lb.h"
+#include "lb_device.cuh"
+#include "lb_internal.h"
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+using lbk::Cols;
+using lbk::Geo;
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  std::vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+#define CU(call)                                                              \
+  do {                                                                        \
+    cudaError_t e_ = (call);                                                  \
+    if (e_ != cudaSuccess)                                                    \
+      return fail(LB_ECUDA, "CUDA error %s at line %d", cudaGetErrorString(e_), __LINE__); \
+  } while (0)
+
+#define NC(call)                                                              \
+  do {                                                                        \
+    ncclResult_t r_ = (call);                                                 \
+    if (r_ != ncclSuccess)                                                    \
+      return fail(LB_ENCCL, "NCCL error %s at line %d", ncclGetErrorString(r_), __LINE__); \
+  } while (0)
+
+constexpr int Y0 = 16;  // internal row of physical row 0: 128-byte aligned
+
+// Host copy of the velocity / weight tables, from the device header's
+// constexpr arrays (one source of truth inside the library).
+double host_weight(int l) { return lbd::SHELL_W(lbd::shell_of(l)); }
+
+// K_wall,l(T_wall), App. B with the canonical expression tree of DESIGN.md
+// §3 (reading G16/G25), evaluated on the host (compiled -ffp-contract=off).
+void kwall(double t_wall, double* K) {
+  const double a = lbd::A_SCALE;
+  const double a2 = a * a;
+  const double t = a2 * t_wall - 1.0;
+  for (int l = 0; l < lbd::Q; ++l) {
+    const double x2 = a2 * (double)(lbd::CX(l) * lbd::CX(l) + lbd::CY(l) * lbd::CY(l));
+    K[l] = host_weight(l) * ((1.0 + (0.5 * t) * (x2 - 2.0)) + ((0.125 * t) * t) * ((x2 * x2 - 8.0 * x2) + 8.0));
+  }
+}
+
+struct ProfEntry {
+  int kernel;
+  cudaEvent_t e0, e1;
+  int64_t units;
+};
+
+}  // namespace
+
+struct lb_ctx {
+  lb_params p{};
+  lb_layout L{};
+  Geo g{};
+  int rank = 0, nranks = 1, left = 0, right = 0;
+  double *A = nullptr, *B = nullptr;
+  cudaStream_t s = nullptr;       // compute stream (caller's)
+  cudaStream_t s_comm = nullptr;  // high-priority exchange stream
+  cudaEvent_t ev_ready = nullptr, ev_comm = nullptr;
+  ncclComm_t comm = nullptr;
+  double* d_part = nullptr;   // invariants partials (+5 result doubles)
+  double* h_pin = nullptr;    // pinned 8 doubles for results
+  int phase = 0;              // 0 = step boundary, 1 = after propagate, 2 = after bc
+  double omega = 1.0;
+  int64_t launches = 0;
+  // instrumentation
+  bool prof = false;
+  std::vector<std::string> knames;
+  std::vector<ProfEntry> pending;
+  std::vector<cudaEvent_t> evpool;
+  std::vector<double> kms;
+  std::vector<int64_t> kcount, kunits;
+};
+
+namespace {
+
+int kernel_id(lb_ctx* c, const char* name) {
+  for (size_t i = 0; i < c->knames.size(); ++i)
+    if (c->knames[i] == name) return (int)i;
+  c->knames.emplace_back(name);
+  c->kms.push_back(0.0);
+  c->kcount.push_back(0);
+  c->kunits.push_back(0);
+  return (int)c->knames.size() - 1;
+}
+
+cudaEvent_t get_event(lb_ctx* c) {
+  if (!c->evpool.empty()) {
+    cudaEvent_t e = c->evpool.back();
+    c->evpool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+int harvest(lb_ctx* c) {
+  for (auto& pe : c->pending) {
+    CU(cudaEventSynchronize(pe.e1));
+    float ms = 0.f;
+    CU(cudaEventElapsedTime(&ms, pe.e0, pe.e1));
+    c->kms[pe.kernel] += ms;
+    c->kcount[pe.kernel] += 1;
+    c->kunits[pe.kernel] += pe.units;
+    c->evpool.push_back(pe.e0);
+    c->evpool.push_back(pe.e1);
+  }
+  c->pending.clear();
+  return LB_OK;
+}
+
+// Launch wrapper: counts launches and, when profiling, brackets the launch
+// with events on the stream it is enqueued on.
+template <class F>
+int launch(lb_ctx* c, const char* name, cudaStream_t s, int64_t units, F&& f) {
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (c->prof) {
+    e0 = get_event(c);
+    e1 = get_event(c);
+    CU(cudaEventRecord(e0, s));
+  }
+  cudaError_t e = f();
+  if (e != cudaSuccess) return fail(LB_ECUDA, "launch of %s failed: %s", name, cudaGetErrorString(e));
+  c->launches++;
+  if (c->prof) {
+    CU(cudaEventRecord(e1, s));
+    c->pending.push_back({kernel_id(c, name), e0, e1, units});
+    if (c->pending.size() > 8192) return harvest(c);
+  }
+  return LB_OK;
+}
+
+#define TRY(x)                  \
+  do {                          \
+    int r_ = (x);               \
+    if (r_ != LB_OK) return r_; \
+  } while (0)
+
+int validate(const lb_params* p, int rank, int nranks) {
+  if (!p) return fail(LB_EINVAL, "params is NULL");
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(LB_EINVAL, "bad rank %d / nranks %d", rank, nranks);
+  if (p->lx_total <= 0 || p->lx_total % nranks) return fail(LB_EINVAL, "lx_total %% nranks != 0");
+  const int lx = p->lx_total / nranks;
+  if (lx < (nranks == 1 ? 3 : 6)) return fail(LB_EINVAL, "per-rank lx = %d too small", lx);
+  if (p->bc_y < 0 || p->bc_y > 2) return fail(LB_EINVAL, "bad bc_y");
+  if (p->ly < (p->bc_y == LB_PERIODIC ? 3 : 6)) return fail(LB_EINVAL, "ly = %d too small", p->ly);
+  if (p->mode < 0 || p->mode > 1) return fail(LB_EINVAL, "bad mode");
+  if (!(p->tau > 0.0) || !(p->dt > 0.0)) return fail(LB_EINVAL, "tau and dt must be > 0");
+  const double om = p->dt / p->tau;
+  if (!(om > 0.0 && om <= 2.0)) return fail(LB_EINVAL, "dt/tau must be in (0, 2]");
+  if (p->bc_y == LB_WALL_THERMAL && !(p->t_bottom > 0.0 && p->t_top > 0.0))
+    return fail(LB_EINVAL, "wall temperatures must be > 0");
+  const int64_t nyp = ((int64_t)Y0 + p->ly + 3 + 15) / 16 * 16;
+  if (nyp * 37 * 3 > (int64_t)1 << 30) return fail(LB_EINVAL, "ly too large");
+  return LB_OK;
+}
+
+void fill_layout(const lb_params* p, int rank, int nranks, lb_layout* L) {
+  L->lx = p->lx_total / nranks;
+  L->ly = p->ly;
+  L->nx = L->lx + 2 * LB_HALO;
+  L->y0 = Y0;
+  L->nyp = (int)(((int64_t)Y0 + p->ly + 3 + 15) / 16 * 16);
+  L->x0_global = rank * L->lx;
+  L->col_stride = (int64_t)37 * L->nyp;
+  L->elems = (int64_t)L->nx * L->col_stride;
+  L->bytes = L->elems * 8;
+  L->sites = (int64_t)L->lx * L->ly;
+}
+
+Cols all_cols(const lb_ctx* c) { return Cols{LB_HALO, LB_HALO + c->g.lx, 0, 0}; }
+Cols bulk_cols(const lb_ctx* c) { return Cols{LB_HALO + 3, LB_HALO + c->g.lx - 3, 0, 0}; }
+Cols border_cols(const lb_ctx* c) {
+  return Cols{LB_HALO, LB_HALO + 3, LB_HALO + c->g.lx - 3, LB_HALO + c->g.lx};
+}
+
+// ---- exchange (§8a1) -------------------------------------------------------
+// N = 1: local wrap kernel on stream s.  N > 1: grouped NCCL send/recv of the
+// contiguous 3-column blocks on the ring.  For a pair of
+// ranks the sends are posted (to right, to left) and the receives (from left,
+// from right), so for N = 2 (left == right) the k-th send matches the k-th
+// receive of the peer in the right halo.
+int exchange_on(lb_ctx* c, cudaStream_t s) {
+  const Geo& g = c->g;
+  if (c->nranks == 1) {
+    return launch(c, "k_pbc_wrap", s, 6LL * g.ly, [&] {
+      return lbk::launch_pbc_wrap(g, c->A, c->p.bc_y, s);
+    });
+  }
+  const size_t n = (size_t)3 * g.cs;
+  double* halo_l = c->A;
+  double* halo_r = c->A + (int64_t)(g.lx + 3) * g.cs;
+  double* bord_l = c->A + (int64_t)3 * g.cs;
+  double* bord_r = c->A + (int64_t)g.lx * g.cs;
+  NC(ncclGroupStart());
+  NC(ncclRecv(halo_l, n, ncclDouble, c->left, c->comm, s));
+  NC(ncclRecv(halo_r, n, ncclDouble, c->right, c->comm, s));
+  NC(ncclSend(bord_r, n, ncclDouble, c->right, c->comm, s));
+  NC(ncclSend(bord_l, n, ncclDouble, c->left, c->comm, s));
+  NC(ncclGroupEnd());
+  if (c->p.bc_y == LB_PERIODIC)
+    TRY(launch(c, "k_ywrap", s, 0, [&] { return lbk::launch_ywrap(g, c->A, s); }));
+  return LB_OK;
+}
+
+int fused(lb_ctx* c, Cols cols) {
+  return launch(c, "k_step_fused", c->s, (int64_t)cols.count() * c->g.ly, [&] {
+    return lbk::launch_step_fused(c->g, c->A, c->B, c->p.bc_y, c->omega, cols, c->s);
+  });
+}
+
+int step_once(lb_ctx* c) {
+  const bool overlap = c->p.overlap && c->p.mode == LB_MODE_FUSED && c->g.lx >= 6 &&
+                       !(c->p.bc_y == LB_PERIODIC && c->nranks > 1);
+  if (c->p.mode == LB_MODE_SPLIT) {
+    TRY(lb_exchange(c));
+    TRY(lb_propagate(c));
+    TRY(lb_bc(c));
+    return lb_collide(c);
+  }
+  if (!overlap) {
+    TRY(lb_exchange(c));
+    TRY(fused(c, all_cols(c)));
+  } else {
+    // bulk || exchange, then borders.  A is read-only
+    // during the step (G11), so the bulk and the exchange never race.
+    CU(cudaEventRecord(c->ev_ready, c->s));
+    CU(cudaStreamWaitEvent(c->s_comm, c->ev_ready, 0));
+    TRY(exchange_on(c, c->s_comm));
+    CU(cudaEventRecord(c->ev_comm, c->s_comm));
+    TRY(fused(c, bulk_cols(c)));
+    CU(cudaStreamWaitEvent(c->s, c->ev_comm, 0));
+    TRY(fused(c, border_cols(c)));
+  }
+  std::swap(c->A, c->B);
+  return LB_OK;
+}
+
+Geo make_geo(const lb_layout& L) {
+  Geo g;
+  g.lx = L.lx;
+  g.ly = L.ly;
+  g.nx = L.nx;
+  g.nyp = L.nyp;
+  g.y0 = L.y0;
+  g.cs = L.col_stride;
+  return g;
+}
+
+int check_boundary(lb_ctx* c, const char* what) {
+  if (!c) return fail(LB_EINVAL, "ctx is NULL");
+  if (c->phase != 0) return fail(LB_ESTATE, "%s is only allowed at a step boundary (phase %d)", what, c->phase);
+  return LB_OK;
+}
+
+}  // namespace
+
+// ============================================================================
+extern "C" {
+
+const char* lb_last_error(void) { return g_err; }
+
+const char* lb_strerror(int s) {
+  switch (s) {
+    case LB_OK: return "ok";
+    case LB_EINVAL: return "invalid argument";
+    case LB_ESTATE: return "call out of order";
+    case LB_ECUDA: return "CUDA error";
+    case LB_ENCCL: return "NCCL error";
+    case LB_ENONPHYS: return "non-physical state (NaN or rho <= 0)";
+    case LB_ENOMEM: return "out of memory";
+    default: return "unknown status";
+  }
+}
+
+int lb_query_layout(const lb_params* p, int rank, int nranks, lb_layout* out) {
+  TRY(validate(p, rank, nranks));
+  if (!out) return fail(LB_EINVAL, "out is NULL");
+  fill_layout(p, rank, nranks, out);
+  return LB_OK;
+}
+
+int lb_constants(int* c, double* w, double* a, double* t0) {
+  for (int l = 0; l < lbd::Q; ++l) {
+    if (c) {
+      c[2 * l] = lbd::CX(l);
+      c[2 * l + 1] = lbd::CY(l);
+    }
+    if (w) w[l] = host_weight(l);
+  }
+  if (a) *a = lbd::A_SCALE;
+  if (t0) *t0 = 1.0 / (lbd::A_SCALE * lbd::A_SCALE);
+  return LB_OK;
+}
+
+int lb_kwall(double t_wall, double* K) {
+  if (!K) return fail(LB_EINVAL, "K is NULL");
+  kwall(t_wall, K);
+  return LB_OK;
+}
+
+int lb_nccl_unique_id(unsigned char* out) {
+  if (!out) return fail(LB_EINVAL, "out is NULL");
+  ncclUniqueId id;
+  NC(ncclGetUniqueId(&id));
+  static_assert(sizeof(id) == 128, "ncclUniqueId size");
+  std::memcpy(out, &id, 128);
+  return LB_OK;
+}
+
+int lb_init(const lb_params* p, const lb_dist* d, double* f_a, double* f_b, void* stream,
+            lb_ctx** out) {
+  if (!out) return fail(LB_EINVAL, "out is NULL");
+  *out = nullptr;
+  const int rank = d ? d->rank : 0, nranks = d ? d->nranks : 1;
+  TRY(validate(p, rank, nranks));
+  if (!f_a || !f_b || f_a == f_b) return fail(LB_EINVAL, "need two distinct device buffers");
+  if (((uintptr_t)f_a | (uintptr_t)f_b) & 15) return fail(LB_EINVAL, "buffers must be 16-byte aligned");
+  if (nranks > 1 && (!d || !d->nccl_id)) return fail(LB_EINVAL, "nranks > 1 needs an nccl_id");
+  lb_ctx* c = new (std::nothrow) lb_ctx();
+  if (!c) return fail(LB_ENOMEM, "host allocation failed");
+  c->p = *p;
+  fill_layout(p, rank, nranks, &c->L);
+  c->g = make_geo(c->L);
+  c->rank = rank;
+  c->nranks = nranks;
+  c->left = (rank - 1 + nranks) % nranks;
+  c->right = (rank + 1) % nranks;
+  c->A = f_a;
+  c->B = f_b;
+  c->s = (cudaStream_t)stream;
+  c->omega = p->dt / p->tau;
+  auto bail = [&](int code) {
+    lb_destroy(c);
+    return code;
+  };
+  int lo = 0, hi = 0;
+  if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess ||
+      cudaStreamCreateWithPriority(&c->s_comm, cudaStreamNonBlocking, hi) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_comm, cudaEventDisableTiming) != cudaSuccess)
+    return bail(fail(LB_ECUDA, "stream/event creation failed"));
+  const size_t npart = lbk::invariants_scratch(c->g) + 8;
+  if (cudaMalloc(&c->d_part, npart * sizeof(double)) != cudaSuccess)
+    return bail(fail(LB_ENOMEM, "device scratch allocation failed"));
+  if (cudaMallocHost(&c->h_pin, 16 * sizeof(double)) != cudaSuccess)
+    return bail(fail(LB_ENOMEM, "pinned allocation failed"));
+  if (cudaMemsetAsync(c->A, 0, c->L.bytes, c->s) != cudaSuccess ||
+      cudaMemsetAsync(c->B, 0, c->L.bytes, c->s) != cudaSuccess)
+    return bail(fail(LB_ECUDA, "zero-fill failed: %s", cudaGetErrorString(cudaGetLastError())));
+  double kb[lbd::Q], kt[lbd::Q];
+  kwall(p->t_bottom, kb);
+  kwall(p->t_top, kt);
+  if (lbk::upload_kwall(kb, kt, c->s) != cudaSuccess)
+    return bail(fail(LB_ECUDA, "constant upload failed"));
+  if (nranks > 1) {
+    ncclUniqueId id;
+    std::memcpy(&id, d->nccl_id, 128);
+    ncclResult_t r = ncclCommInitRank(&c->comm, nranks, id, rank);
+    if (r != ncclSuccess) return bail(fail(LB_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r)));
+  }
+  if (cudaStreamSynchronize(c->s) != cudaSuccess)
+    return bail(fail(LB_ECUDA, "init sync failed: %s", cudaGetErrorString(cudaGetLastError())));
+  *out = c;
+  return LB_OK;
+}
+
+void lb_destroy(lb_ctx* c) {
+  if (!c) return;
+  if (c->s) cudaStreamSynchronize(c->s);
+  if (c->s_comm) cudaStreamSynchronize(c->s_comm);
+  for (auto& pe : c->pending) {
+    cudaEventDestroy(pe.e0);
+    cudaEventDestroy(pe.e1);
+  }
+  for (auto e : c->evpool) cudaEventDestroy(e);
+  if (c->comm) ncclCommDestroy(c->comm);
+  if (c->ev_ready) cudaEventDestroy(c->ev_ready);
+  if (c->ev_comm) cudaEventDestroy(c->ev_comm);
+  if (c->s_comm) cudaStreamDestroy(c->s_comm);
+  if (c->d_part) cudaFree(c->d_part);
+  if (c->h_pin) cudaFreeHost(c->h_pin);
+  delete c;
+}
+
+int lb_get_layout(const lb_ctx* c, lb_layout* out) {
+  if (!c || !out) return fail(LB_EINVAL, "NULL argument");
+  *out = c->L;
+  return LB_OK;
+}
+
+int lb_set_stream(lb_ctx* c, void* stream) {
+  if (!c) return fail(LB_EINVAL, "ctx is NULL");
+  c->s = (cudaStream_t)stream;
+  return LB_OK;
+}
+
+int lb_init_macro(lb_ctx* c, const double* rho, const double* ux, const double* uy,
+                  const double* T, int on_device) {
+  TRY(check_boundary(c, "lb_init_macro"));
+  if (!rho || !ux || !uy || !T) return fail(LB_EINVAL, "NULL field");
+  const int64_t n = c->L.sites;
+  const double* src[4] = {rho, ux, uy, T};
+  const double* dev[4];
+  for (int k = 0; k < 4; ++k) {
+    if (on_device) {
+      dev[k] = src[k];
+    } else {
+      double* dst = c->B + k * n;  // B is scratch at a step boundary
+      CU(cudaMemcpyAsync(dst, src[k], n * sizeof(double), cudaMemcpyHostToDevice, c->s));
+      dev[k] = dst;
+    }
+  }
+  TRY(launch(c, "k_init_macro", c->s, n, [&] {
+    return lbk::launch_init_macro(c->g, c->A, dev[0], dev[1], dev[2], dev[3], c->s);
+  }));
+  if (!on_device) CU(cudaMemsetAsync(c->B, 0, c->L.bytes, c->s));
+  return LB_OK;
+}
+
+int lb_set_state(lb_ctx* c, const double* canon, int on_device) {
+  TRY(check_boundary(c, "lb_set_state"));
+  if (!canon) return fail(LB_EINVAL, "NULL state");
+  const int64_t n = (int64_t)37 * c->L.sites;
+  const double* src = canon;
+  if (!on_device) {
+    CU(cudaMemcpyAsync(c->B, canon, n * sizeof(double), cudaMemcpyHostToDevice, c->s));
+    src = c->B;
+  }
+  TRY(launch(c, "k_canon_to_internal", c->s, c->L.sites, [&] {
+    return lbk::launch_canon_to_internal(c->g, src, c->A, c->s);
+  }));
+  if (!on_device) CU(cudaMemsetAsync(c->B, 0, c->L.bytes, c->s));
+  return LB_OK;
+}
+
+int lb_exchange(lb_ctx* c) {
+  TRY(check_boundary(c, "lb_exchange"));
+  if (c->nranks == 1) return exchange_on(c, c->s);
+  CU(cudaEventRecord(c->ev_ready, c->s));
+  CU(cudaStreamWaitEvent(c->s_comm, c->ev_ready, 0));
+  TRY(exchange_on(c, c->s_comm));
+  CU(cudaEventRecord(c->ev_comm, c->s_comm));
+  CU(cudaStreamWaitEvent(c->s, c->ev_comm, 0));
+  return LB_OK;
+}
+
+int lb_propagate(lb_ctx* c) {
+  TRY(check_boundary(c, "lb_propagate"));
+  TRY(launch(c, "k_propagate", c->s, c->L.sites, [&] {
+    return lbk::launch_propagate(c->g, c->A, c->B, c->s);
+  }));
+  c->phase = 1;
+  return LB_OK;
+}
+
+int lb_bc(lb_ctx* c) {
+  if (!c) return fail(LB_EINVAL, "ctx is NULL");
+  if (c->phase != 1) return fail(LB_ESTATE, "lb_bc must follow lb_propagate");
+  if (c->p.bc_y != LB_PERIODIC)
+    TRY(launch(c, "k_bc", c->s, 6LL * c->g.lx, [&] {
+      return lbk::launch_bc(c->g, c->A, c->B, c->p.bc_y, c->s);
+    }));
+  c->phase = 2;
+  return LB_OK;
+}
+
+int lb_collide(lb_ctx* c) {
+  if (!c) return fail(LB_EINVAL, "ctx is NULL");
+  if (c->phase != 2 && !(c->phase == 1 && c->p.bc_y == LB_PERIODIC))
+    return fail(LB_ESTATE, "lb_collide must follow lb_bc");
+  TRY(launch(c, "k_collide", c->s, c->L.sites, [&] {
+    return lbk::launch_collide(c->g, c->B, c->omega, c->s);
+  }));
+  std::swap(c->A, c->B);
+  c->phase = 0;
+  return LB_OK;
+}
+
+int lb_step(lb_ctx* c, int nsteps) {
+  TRY(check_boundary(c, "lb_step"));
+  if (nsteps < 0) return fail(LB_EINVAL, "nsteps < 0");
+  for (int k = 0; k < nsteps; ++k) TRY(step_once(c));
+  return LB_OK;
+}
+
+int lb_sync(lb_ctx* c) {
+  if (!c) return fail(LB_EINVAL, "ctx is NULL");
+  CU(cudaStreamSynchronize(c->s));
+  CU(cudaStreamSynchronize(c->s_comm));
+  return LB_OK;
+}
+
+int lb_gather(lb_ctx* c, double* host_out, int root) {
+  TRY(check_boundary(c, "lb_gather"));
+  if (root < 0 || root >= c->nranks) return fail(LB_EINVAL, "bad root %d", root);
+  if (c->rank == root && !host_out) return fail(LB_EINVAL, "host_out is NULL on root");
+  const Geo& g = c->g;
+  const int64_t blk = (int64_t)g.lx * g.ly;  // one plane of one rank
+  const size_t dpitch = (size_t)c->p.lx_total * g.ly * sizeof(double);
+  TRY(launch(c, "k_internal_to_canon", c->s, c->L.sites, [&] {
+    return lbk::launch_internal_to_canon(g, c->A, c->B, c->s);
+  }));
+  if (c->rank == root) {
+    CU(cudaMemcpy2DAsync(host_out + (int64_t)c->rank * blk, dpitch, c->B, blk * sizeof(double),
+                         blk * sizeof(double), 37, cudaMemcpyDeviceToHost, c->s));
+    CU(cudaStreamSynchronize(c->s));
+    for (int r = 0; r < c->nranks; ++r) {
+      if (r == root) continue;
+      NC(ncclRecv(c->B, (size_t)37 * blk, ncclDouble, r, c->comm, c->s));
+      CU(cudaMemcpy2DAsync(host_out + (int64_t)r * blk, dpitch, c->B, blk * sizeof(double),
+                           blk * sizeof(double), 37, cudaMemcpyDeviceToHost, c->s));
+      CU(cudaStreamSynchronize(c->s));
+    }
+  } else {
+    NC(ncclSend(c->B, (size_t)37 * blk, ncclDouble, root, c->comm, c->s));
+  }
+  CU(cudaMemsetAsync(c->B, 0, c->L.bytes, c->s));  // restore zero halo rows (G10)
+  CU(cudaStreamSynchronize(c->s));
+  return LB_OK;
+}
+
+int lb_peek(lb_ctx* c, int which, double* host_out) {
+  if (!c || !host_out || (which != 0 && which != 1)) return fail(LB_EINVAL, "bad argument");
+  const Geo& g = c->g;
+  std::vector<double> buf;
+  try {
+    buf.resize((size_t)c->L.elems);
+  } catch (...) {
+    return fail(LB_ENOMEM, "host staging allocation failed");
+  }
+  CU(cudaStreamSynchronize(c->s_comm));
+  CU(cudaMemcpyAsync(buf.data(), which ? c->B : c->A, c->L.bytes, cudaMemcpyDeviceToHost, c->s));
+  CU(cudaStreamSynchronize(c->s));
+  for (int l = 0; l < 37; ++l)
+    for (int x = 0; x < g.lx; ++x)
+      std::memcpy(host_out + ((int64_t)l * g.lx + x) * g.ly,
+                  buf.data() + (int64_t)(x + 3) * g.cs + (int64_t)l * g.nyp + g.y0,
+                  sizeof(double) * g.ly);
+  return LB_OK;
+}
+
+int lb_invariants(lb_ctx* c, double* out) {
+  TRY(check_boundary(c, "lb_invariants"));
+  if (!out) return fail(LB_EINVAL, "out is NULL");
+  double* res = c->d_part + lbk::invariants_scratch(c->g);
+  TRY(launch(c, "k_invariants", c->s, c->L.sites, [&] {
+    return lbk::launch_invariants(c->g, c->A, c->d_part, res, c->s);
+  }));
+  if (c->nranks > 1) {
+    NC(ncclGroupStart());
+    NC(ncclAllReduce(res, res, 4, ncclDouble, ncclSum, c->comm, c->s));
+    NC(ncclAllReduce(res + 4, res + 4, 1, ncclDouble, ncclMin, c->comm, c->s));
+    NC(ncclGroupEnd());
+  }
+  CU(cudaMemcpyAsync(c->h_pin, res, 5 * sizeof(double), cudaMemcpyDeviceToHost, c->s));
+  CU(cudaStreamSynchronize(c->s));
+  std::memcpy(out, c->h_pin, 5 * sizeof(double));
+  for (int k = 0; k < 5; ++k)
+    if (std::isnan(out[k])) return fail(LB_ENONPHYS, "NaN in invariants");
+  if (!(out[4] > 0.0)) return fail(LB_ENONPHYS, "site density <= 0 or NaN");
+  return LB_OK;
+}
+
+int lb_profile_enable(lb_ctx* c, int enable) {
+  if (!c) return fail(LB_EINVAL, "ctx is NULL");
+  c->prof = enable != 0;
+  return LB_OK;
+}
+
+int lb_profile_reset(lb_ctx* c) {
+  if (!c) return fail(LB_EINVAL, "ctx is NULL");
+  TRY(harvest(c));
+  std::fill(c->kms.begin(), c->kms.end(), 0.0);
+  std::fill(c->kcount.begin(), c->kcount.end(), 0);
+  std::fill(c->kunits.begin(), c->kunits.end(), 0);
+  return LB_OK;
+}
+
+int lb_profile_read(lb_ctx* c, lb_kprof* out, int max, int* n) {
+  if (!c) return fail(LB_EINVAL, "ctx is NULL");
+  TRY(harvest(c));
+  const int k = (int)c->knames.size();
+  if (n) *n = k;
+  for (int i = 0; i < k && i < max && out; ++i) {
+    std::memset(out[i].name, 0, sizeof(out[i].name));
+    std::strncpy(out[i].name, c->knames[i].c_str(), sizeof(out[i].name) - 1);
+    out[i].launches = c->kcount[i];
+    out[i].total_ms = c->kms[i];
+    out[i].units = c->kunits[i];
+  }
+  return LB_OK;
+}
+
+int64_t lb_launch_count(const lb_ctx* c) { return c ? c->launches : -1; }
+
+}  // extern "C"

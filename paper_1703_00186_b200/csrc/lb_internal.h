@@ -1,0 +1,46 @@
+// lb_internal.h — host-side declarations shared by lb_kernels.cu and lb_api.cu.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace lbk {
+
+// Geometry of one rank's internal buffers (see include/lb.h "internal").
+struct Geo {
+  int lx, ly;      // physical extents
+  int nx;          // lx + 6
+  int nyp;         // padded rows per population column
+  int y0;          // internal row of physical row 0
+  int64_t cs;      // column stride = 37 * nyp
+};
+
+enum BcKind { BC_THERMAL = 0, BC_ADIABATIC = 1, BC_PERIODIC = 2 };
+
+// Column ranges are in internal column indices (physical columns are
+// [3, 3+lx)).  A launch covers [xa0, xa1) U [xb0, xb1).
+struct Cols {
+  int xa0, xa1, xb0, xb1;
+  int count() const { return (xa1 - xa0) + (xb1 - xb0); }
+};
+
+cudaError_t upload_kwall(const double* k_bottom, const double* k_top, cudaStream_t s);
+
+// N=1 periodic wrap of the x-halo columns (and y-halo rows when periodic).
+cudaError_t launch_pbc_wrap(const Geo& g, double* A, int bc, cudaStream_t s);
+// y-halo wrap only (periodic bc, N>1 after the x exchange)
+cudaError_t launch_ywrap(const Geo& g, double* A, cudaStream_t s);
+cudaError_t launch_propagate(const Geo& g, const double* A, double* B, cudaStream_t s);
+cudaError_t launch_bc(const Geo& g, const double* A, double* B, int bc, cudaStream_t s);
+cudaError_t launch_collide(const Geo& g, double* B, double omega, cudaStream_t s);
+cudaError_t launch_step_fused(const Geo& g, const double* A, double* B, int bc, double omega,
+                              Cols cols, cudaStream_t s);
+cudaError_t launch_init_macro(const Geo& g, double* A, const double* rho, const double* ux,
+                              const double* uy, const double* T, cudaStream_t s);
+cudaError_t launch_canon_to_internal(const Geo& g, const double* canon, double* A, cudaStream_t s);
+cudaError_t launch_internal_to_canon(const Geo& g, const double* A, double* canon, cudaStream_t s);
+// partials: scratch of at least invariants_scratch(g) doubles; out: 5 doubles on device
+size_t invariants_scratch(const Geo& g);
+cudaError_t launch_invariants(const Geo& g, const double* A, double* partials, double* out,
+                              cudaStream_t s);
+
+}  // namespace lbk

@@ -1,0 +1,384 @@
+// lb_kernels.cu — sm_100a kernels of the D2Q37 hot path.
+//
+// Memory layout: column-blocked SoA, element (ix, l, r) at (ix*37 + l)*nyp + r
+// (include/lb.h).  Thread mapping for every per-site kernel: one thread per
+// lattice site, a warp covers 32 consecutive rows of one column, so every
+// population access of a warp is one contiguous 256-byte run (coalesced; the
+// +-3 row shift of the pull makes it straddle one extra 32-byte sector, which
+// the neighbouring warp uses — DRAM traffic stays at 1x).
+//
+// None of these kernels is a dense contraction, so there is no tensor-core
+// path (SURVEY.md §2 "Hardware"); propagate / fused are HBM-bound, collide's
+// FP64 work sits on the FP64 pipe with all constants as immediates or
+// constant-bank operands.
+#include "lb_device.cuh"
+#include "lb_internal.h"
+
+namespace lbd {
+// Wall constants K_wall,l for the bottom (0) and top (1) wall; computed on
+// the host with the canonical expression tree (G16) and uploaded by lb_init.
+__constant__ double c_kwall[2][Q];
+
+// Thermal wall repopulation (G9 ii): rho = ((f0 + f1) + f2) + ... + f36
+// sequentially, then f_l = rho * K_l — the expression tree of DESIGN.md §3.
+__device__ __forceinline__ void thermal_wall(double (&f)[Q], int wall) {
+  double rho = f[0];
+#pragma unroll
+  for (int l = 1; l < Q; ++l) rho = dadd(rho, f[l]);
+#pragma unroll
+  for (int l = 0; l < Q; ++l) f[l] = dmul(rho, c_kwall[wall][l]);
+}
+
+}
+
+namespace lbk {
+using namespace lbd;
+
+constexpr int TPB = 128;  // threads per block of the per-site kernels
+
+cudaError_t upload_kwall(const double* k_bottom, const double* k_top, cudaStream_t s) {
+  cudaError_t e = cudaMemcpyToSymbolAsync(c_kwall, k_bottom, sizeof(double) * Q, 0,
+                                          cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return e;
+  e = cudaMemcpyToSymbolAsync(c_kwall, k_top, sizeof(double) * Q, sizeof(double) * Q,
+                              cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return e;
+  return cudaStreamSynchronize(s);
+}
+
+// ---------------------------------------------------------------- pbc (§8a1)
+// N=1 wrap: halo columns [0,3) <- [lx, lx+3), [lx+3, lx+6) <- [3, 6),
+// full columns including the y-halo rows (G12).  Column blocks are contiguous,
+// so this is two 16-byte-vectorised block copies.
+__global__ void __launch_bounds__(256) k_pbc_wrap(double2* __restrict__ A, int64_t lx, int64_t cs2) {
+  const int64_t n = 3 * cs2;  // double2 per side
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 2 * n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < n)
+      A[i] = A[lx * cs2 + i];                       // left halo <- rightmost physical
+    else
+      A[(lx + 3) * cs2 + (i - n)] = A[3 * cs2 + (i - n)];  // right halo <- leftmost physical
+  }
+}
+
+// Periodic-Y wrap of the y-halo rows of every column (test geometry only).
+__global__ void k_ywrap(double* __restrict__ A, Geo g) {
+  const int64_t ncl = (int64_t)g.nx * Q;  // (column, population) pairs
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ncl * 6;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t cl = i / 6;
+    const int j = (int)(i % 6);
+    double* col = A + cl * g.nyp + g.y0;
+    if (j < 3)
+      col[j - 3] = col[g.ly + j - 3];      // rows -3..-1 <- ly-3..ly-1
+    else
+      col[g.ly + (j - 3)] = col[j - 3];    // rows ly..ly+2 <- 0..2
+  }
+}
+
+cudaError_t launch_pbc_wrap(const Geo& g, double* A, int bc, cudaStream_t s) {
+  const int64_t cs2 = g.cs / 2;
+  int blocks = (int)std::min<int64_t>((6 * cs2 + 255) / 256, 148 * 8);
+  k_pbc_wrap<<<blocks, 256, 0, s>>>(reinterpret_cast<double2*>(A), g.lx, cs2);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || bc != BC_PERIODIC) return e;
+  return launch_ywrap(g, A, s);
+}
+
+cudaError_t launch_ywrap(const Geo& g, double* A, cudaStream_t s) {
+  const int64_t n = (int64_t)g.nx * Q * 6;
+  int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+  k_ywrap<<<blocks, 256, 0, s>>>(A, g);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- gather
+// Pull of the 37 populations of site (ix, y) from A (Eq. 1):
+// f_l = A[ix - cx_l, l, y - cy_l].  With MIRROR, a source row beyond a wall
+// (walls at y = -1/2 and y = ly - 1/2) is replaced by the specular image
+// (G9 i): population refl(l) at row -1 - sy (bottom) or 2 ly - 1 - sy (top).
+template <bool MIRROR>
+__device__ __forceinline__ void gather(const double* __restrict__ A, const Geo& g, int ix, int y,
+                                       double (&f)[Q]) {
+  const int64_t b = (int64_t)ix * g.cs + g.y0 + y;
+#pragma unroll
+  for (int l = 0; l < Q; ++l) {
+    int plane = l;
+    int dy = -CY(l);
+    if (MIRROR) {
+      const int sy = y - CY(l);
+      if (sy < 0) { plane = refl(l); dy = (-1 - sy) - y; }
+      else if (sy >= g.ly) { plane = refl(l); dy = (2 * g.ly - 1 - sy) - y; }
+    }
+    const int64_t off = (int64_t)plane * g.nyp - (int64_t)CX(l) * g.cs + dy;
+    f[l] = __ldg(A + b + off);
+  }
+}
+
+__device__ __forceinline__ void store_site(double* __restrict__ B, const Geo& g, int ix, int y,
+                                           const double (&f)[Q]) {
+  double* p = B + (int64_t)ix * g.cs + g.y0 + y;
+#pragma unroll
+  for (int l = 0; l < Q; ++l) p[(int64_t)l * g.nyp] = f[l];
+}
+
+// ---------------------------------------------------------------- propagate (§8a2)
+// Raw pull over all physical sites; entries pulled from the y-halo rows read
+// whatever those rows hold (zeros under walls, G10; wrapped rows if periodic).
+__global__ void __launch_bounds__(TPB) k_propagate(const double* __restrict__ A,
+                                                   double* __restrict__ B, Geo g) {
+  const int y = blockIdx.x * TPB + threadIdx.x;
+  const int ix = H + blockIdx.y;
+  if (y >= g.ly) return;
+  double f[Q];
+  gather<false>(A, g, ix, y, f);
+  store_site(B, g, ix, y, f);
+}
+
+cudaError_t launch_propagate(const Geo& g, const double* A, double* B, cudaStream_t s) {
+  dim3 grid((g.ly + TPB - 1) / TPB, g.lx);
+  k_propagate<<<grid, TPB, 0, s>>>(A, B, g);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- bc (§8a3)
+// One thread per wall-band site (3 rows per wall: both walls in
+// one launch, they touch disjoint rows).  (i) mirror: for every population
+// whose pull source lies beyond the wall, B <- A[refl, ix - cx, image row];
+// (ii) thermal: rho = sequential sum, B_l <- rho K_l.
+template <int BC>
+__global__ void __launch_bounds__(TPB) k_bc(const double* __restrict__ A, double* __restrict__ B,
+                                            Geo g) {
+  const int t = blockIdx.x * TPB + threadIdx.x;
+  if (t >= g.lx * 6) return;
+  const int ix = H + t / 6;
+  const int j = t % 6;
+  const int y = j < 3 ? j : g.ly - 6 + j;
+  double* p = B + (int64_t)ix * g.cs + g.y0 + y;
+#pragma unroll
+  for (int l = 0; l < Q; ++l) {
+    const int sy = y - CY(l);
+    int ys;
+    if (sy < 0) ys = -1 - sy;
+    else if (sy >= g.ly) ys = 2 * g.ly - 1 - sy;
+    else continue;
+    p[(int64_t)l * g.nyp] =
+        A[(int64_t)(ix - CX(l)) * g.cs + (int64_t)refl(l) * g.nyp + g.y0 + ys];
+  }
+  if (BC == BC_THERMAL) {
+    double f[Q];
+#pragma unroll
+    for (int l = 0; l < Q; ++l) f[l] = p[(int64_t)l * g.nyp];
+    thermal_wall(f, j < 3 ? 0 : 1);
+#pragma unroll
+    for (int l = 0; l < Q; ++l) p[(int64_t)l * g.nyp] = f[l];
+  }
+}
+
+cudaError_t launch_bc(const Geo& g, const double* A, double* B, int bc, cudaStream_t s) {
+  if (bc == BC_PERIODIC) return cudaSuccess;
+  const int n = g.lx * 6;
+  const int blocks = (n + TPB - 1) / TPB;
+  if (bc == BC_THERMAL)
+    k_bc<BC_THERMAL><<<blocks, TPB, 0, s>>>(A, B, g);
+  else
+    k_bc<BC_ADIABATIC><<<blocks, TPB, 0, s>>>(A, B, g);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- collide (§8a4)
+__global__ void __launch_bounds__(TPB) k_collide(double* __restrict__ B, Geo g, double omega,
+                                                 double one_m_omega) {
+  const int y = blockIdx.x * TPB + threadIdx.x;
+  const int ix = H + blockIdx.y;
+  if (y >= g.ly) return;
+  double* p = B + (int64_t)ix * g.cs + g.y0 + y;
+  double f[Q];
+#pragma unroll
+  for (int l = 0; l < Q; ++l) f[l] = p[(int64_t)l * g.nyp];
+  collide_site(f, omega, one_m_omega);
+#pragma unroll
+  for (int l = 0; l < Q; ++l) p[(int64_t)l * g.nyp] = f[l];
+}
+
+cudaError_t launch_collide(const Geo& g, double* B, double omega, cudaStream_t s) {
+  dim3 grid((g.ly + TPB - 1) / TPB, g.lx);
+  k_collide<<<grid, TPB, 0, s>>>(B, g, omega, 1.0 - omega);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- fused pull step (§8a5)
+// gather (+mirror) -> thermal wall -> collide -> store, A -> B in one pass:
+// 296 B read + 296 B written per site.  Warps whose 32 rows are all at least
+// 3 rows from both walls take the mirror-free gather (warp-uniform branch).
+template <int BC>
+__global__ void __launch_bounds__(TPB) k_step_fused(const double* __restrict__ A,
+                                                    double* __restrict__ B, Geo g, Cols cols,
+                                                    double omega, double one_m_omega) {
+  const int y = blockIdx.x * TPB + threadIdx.x;
+  const int na = cols.xa1 - cols.xa0;
+  const int ix = (int)blockIdx.y < na ? cols.xa0 + (int)blockIdx.y : cols.xb0 + ((int)blockIdx.y - na);
+  if (y >= g.ly) return;
+  double f[Q];
+  if (BC == BC_PERIODIC) {
+    gather<false>(A, g, ix, y, f);
+  } else {
+    const int wy0 = blockIdx.x * TPB + (threadIdx.x & ~31);
+    const bool interior = (wy0 >= 3) && (wy0 + 32 <= g.ly - 3);
+    if (interior) {
+      gather<false>(A, g, ix, y, f);
+    } else {
+      gather<true>(A, g, ix, y, f);
+      if (BC == BC_THERMAL && (y < 3 || y >= g.ly - 3)) thermal_wall(f, y < 3 ? 0 : 1);
+    }
+  }
+  collide_site(f, omega, one_m_omega);
+  store_site(B, g, ix, y, f);
+}
+
+cudaError_t launch_step_fused(const Geo& g, const double* A, double* B, int bc, double omega,
+                              Cols cols, cudaStream_t s) {
+  const int n = cols.count();
+  if (n <= 0) return cudaSuccess;
+  dim3 grid((g.ly + TPB - 1) / TPB, n);
+  const double om1 = 1.0 - omega;
+  switch (bc) {
+    case BC_THERMAL: k_step_fused<BC_THERMAL><<<grid, TPB, 0, s>>>(A, B, g, cols, omega, om1); break;
+    case BC_ADIABATIC: k_step_fused<BC_ADIABATIC><<<grid, TPB, 0, s>>>(A, B, g, cols, omega, om1); break;
+    default: k_step_fused<BC_PERIODIC><<<grid, TPB, 0, s>>>(A, B, g, cols, omega, om1); break;
+  }
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- init / layout
+// A := f_eq(rho, u, T) on physical sites; macro fields are [lx][ly].
+__global__ void __launch_bounds__(TPB) k_init_macro(double* __restrict__ A, Geo g,
+                                                    const double* __restrict__ rho,
+                                                    const double* __restrict__ ux,
+                                                    const double* __restrict__ uy,
+                                                    const double* __restrict__ T) {
+  const int y = blockIdx.x * TPB + threadIdx.x;
+  const int x = blockIdx.y;
+  if (y >= g.ly) return;
+  const int64_t m = (int64_t)x * g.ly + y;
+  double f[Q];
+  feq_site(rho[m], ux[m], uy[m], T[m], f);
+  store_site(A, g, H + x, y, f);
+}
+
+cudaError_t launch_init_macro(const Geo& g, double* A, const double* rho, const double* ux,
+                              const double* uy, const double* T, cudaStream_t s) {
+  dim3 grid((g.ly + TPB - 1) / TPB, g.lx);
+  k_init_macro<<<grid, TPB, 0, s>>>(A, g, rho, ux, uy, T);
+  return cudaGetLastError();
+}
+
+// canonical [37][lx][ly] <-> internal physical sites
+__global__ void k_canon_to_internal(const double* __restrict__ C, double* __restrict__ A, Geo g) {
+  const int y = blockIdx.x * blockDim.x + threadIdx.x;
+  const int x = blockIdx.y;
+  const int l = blockIdx.z;
+  if (y >= g.ly) return;
+  A[(int64_t)(H + x) * g.cs + (int64_t)l * g.nyp + g.y0 + y] = C[((int64_t)l * g.lx + x) * g.ly + y];
+}
+
+__global__ void k_internal_to_canon(const double* __restrict__ A, double* __restrict__ C, Geo g) {
+  const int y = blockIdx.x * blockDim.x + threadIdx.x;
+  const int x = blockIdx.y;
+  const int l = blockIdx.z;
+  if (y >= g.ly) return;
+  C[((int64_t)l * g.lx + x) * g.ly + y] = A[(int64_t)(H + x) * g.cs + (int64_t)l * g.nyp + g.y0 + y];
+}
+
+cudaError_t launch_canon_to_internal(const Geo& g, const double* canon, double* A, cudaStream_t s) {
+  dim3 grid((g.ly + 255) / 256, g.lx, Q);
+  k_canon_to_internal<<<grid, 256, 0, s>>>(canon, A, g);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_internal_to_canon(const Geo& g, const double* A, double* canon, cudaStream_t s) {
+  dim3 grid((g.ly + 255) / 256, g.lx, Q);
+  k_internal_to_canon<<<grid, 256, 0, s>>>(A, canon, g);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- invariants
+// Deterministic two-pass reduction: block partials (fixed tree) then one
+// block sums the partials in a fixed order.  Per site: rho, jx, jy,
+// E = 1/2 sum |c|^2 f, and min rho.
+constexpr int RED_TPB = 256;
+
+__device__ __forceinline__ void block_reduce5(double (&v)[5], double* sm) {
+  const int t = threadIdx.x;
+#pragma unroll
+  for (int k = 0; k < 5; ++k) sm[k * RED_TPB + t] = v[k];
+  __syncthreads();
+  for (int w = RED_TPB / 2; w > 0; w >>= 1) {
+    if (t < w) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) sm[k * RED_TPB + t] = sm[k * RED_TPB + t] + sm[k * RED_TPB + t + w];
+      sm[4 * RED_TPB + t] = fmin(sm[4 * RED_TPB + t], sm[4 * RED_TPB + t + w]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int k = 0; k < 5; ++k) v[k] = sm[k * RED_TPB];
+}
+
+__global__ void __launch_bounds__(RED_TPB) k_invariants_partial(const double* __restrict__ A, Geo g,
+                                                                double* __restrict__ part) {
+  __shared__ double sm[5 * RED_TPB];
+  const int ix = H + blockIdx.x;
+  double v[5] = {0.0, 0.0, 0.0, 0.0, INFINITY};
+  for (int y = threadIdx.x; y < g.ly; y += RED_TPB) {
+    const double* p = A + (int64_t)ix * g.cs + g.y0 + y;
+    double rho = 0.0, jx = 0.0, jy = 0.0, e = 0.0;
+#pragma unroll
+    for (int l = 0; l < Q; ++l) {
+      const double f = p[(int64_t)l * g.nyp];
+      rho = __dadd_rn(rho, f);
+      jx = __fma_rn((double)CX(l), f, jx);
+      jy = __fma_rn((double)CY(l), f, jy);
+      e = __fma_rn(0.5 * (double)c2(l), f, e);
+    }
+    v[0] += rho;
+    v[1] += jx;
+    v[2] += jy;
+    v[3] += e;
+    // NaN propagates through fmin only if both are NaN; flag NaN as -inf
+    v[4] = (rho != rho) ? -INFINITY : fmin(v[4], rho);
+  }
+  block_reduce5(v, sm);
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int k = 0; k < 5; ++k) part[(int64_t)blockIdx.x * 5 + k] = v[k];
+}
+
+__global__ void __launch_bounds__(RED_TPB) k_invariants_final(const double* __restrict__ part,
+                                                              int nb, double* __restrict__ out) {
+  __shared__ double sm[5 * RED_TPB];
+  double v[5] = {0.0, 0.0, 0.0, 0.0, INFINITY};
+  for (int b = threadIdx.x; b < nb; b += RED_TPB) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] += part[(int64_t)b * 5 + k];
+    const double m = part[(int64_t)b * 5 + 4];
+    v[4] = (m != m || m == -INFINITY) ? -INFINITY : fmin(v[4], m);
+  }
+  block_reduce5(v, sm);
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int k = 0; k < 5; ++k) out[k] = v[k];
+}
+
+size_t invariants_scratch(const Geo& g) { return (size_t)g.lx * 5; }
+
+cudaError_t launch_invariants(const Geo& g, const double* A, double* partials, double* out,
+                              cudaStream_t s) {
+  k_invariants_partial<<<g.lx, RED_TPB, 0, s>>>(A, g, partials);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  k_invariants_final<<<1, RED_TPB, 0, s>>>(partials, g.lx, out);
+  return cudaGetLastError();
+}
+
+}  // namespace lbk

@@ -1,0 +1,303 @@
+"""Thin Python binding of the C ABI in include/lb.h (argument marshalling only).
+
+Every step of the hot path runs in the CUDA kernels of liblb_d2q37.so; this
+module allocates the two population buffers as torch tensors, passes their
+device pointers and the current torch stream, and maps status codes to
+exceptions.  There is no CPU fallback: if the library is missing or there is
+no CUDA device, construction raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+Q = 37
+HALO = 3
+STATUS = {0: "LB_OK", 1: "LB_EINVAL", 2: "LB_ESTATE", 3: "LB_ECUDA", 4: "LB_ENCCL",
+          5: "LB_ENONPHYS", 6: "LB_ENOMEM"}
+BC = {"thermal": 0, "adiabatic": 1, "periodic": 2}
+MODE = {"fused": 0, "split": 1}
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+SO_PATH = os.path.join(_HERE, "liblb_d2q37.so")
+
+# every symbol include/lb.h declares
+EXPORTS = ["lb_query_layout", "lb_constants", "lb_kwall", "lb_nccl_unique_id", "lb_last_error",
+           "lb_strerror", "lb_init", "lb_destroy", "lb_get_layout", "lb_set_stream", "lb_init_macro",
+           "lb_set_state", "lb_exchange", "lb_propagate", "lb_bc", "lb_collide", "lb_step",
+           "lb_gather", "lb_peek", "lb_invariants", "lb_sync", "lb_profile_enable",
+           "lb_profile_reset", "lb_profile_read", "lb_launch_count"]
+
+
+class LBError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class lb_params(ctypes.Structure):
+    _fields_ = [("lx_total", ctypes.c_int), ("ly", ctypes.c_int), ("tau", ctypes.c_double),
+                ("dt", ctypes.c_double), ("t_bottom", ctypes.c_double), ("t_top", ctypes.c_double),
+                ("bc_y", ctypes.c_int), ("mode", ctypes.c_int), ("overlap", ctypes.c_int)]
+
+
+class lb_dist(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int), ("nranks", ctypes.c_int), ("nccl_id", ctypes.c_void_p)]
+
+
+class lb_layout(ctypes.Structure):
+    _fields_ = [("lx", ctypes.c_int), ("ly", ctypes.c_int), ("nx", ctypes.c_int), ("nyp", ctypes.c_int),
+                ("y0", ctypes.c_int), ("x0_global", ctypes.c_int), ("col_stride", ctypes.c_int64),
+                ("elems", ctypes.c_int64), ("bytes", ctypes.c_int64), ("sites", ctypes.c_int64)]
+
+
+class lb_kprof(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char * 32), ("launches", ctypes.c_int64),
+                ("total_ms", ctypes.c_double), ("units", ctypes.c_int64)]
+
+
+_lib = None
+
+
+def lib():
+    """Load liblb_d2q37.so (building it first if the sources are newer)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    import torch  # noqa: F401  (loads the wheel's libnccl.so.2 / CUDA runtime first)
+    from . import _build
+    if _build.needs_build():
+        _build.build()
+    L = ctypes.CDLL(SO_PATH)
+    p, i, d, vp = ctypes.POINTER, ctypes.c_int, ctypes.c_double, ctypes.c_void_p
+    sig = {
+        "lb_query_layout": (i, [p(lb_params), i, i, p(lb_layout)]),
+        "lb_constants": (i, [vp, vp, vp, vp]),
+        "lb_kwall": (i, [d, vp]),
+        "lb_nccl_unique_id": (i, [vp]),
+        "lb_last_error": (ctypes.c_char_p, []),
+        "lb_strerror": (ctypes.c_char_p, [i]),
+        "lb_init": (i, [p(lb_params), p(lb_dist), vp, vp, vp, p(vp)]),
+        "lb_destroy": (None, [vp]),
+        "lb_get_layout": (i, [vp, p(lb_layout)]),
+        "lb_set_stream": (i, [vp, vp]),
+        "lb_init_macro": (i, [vp, vp, vp, vp, vp, i]),
+        "lb_set_state": (i, [vp, vp, i]),
+        "lb_exchange": (i, [vp]), "lb_propagate": (i, [vp]), "lb_bc": (i, [vp]),
+        "lb_collide": (i, [vp]), "lb_step": (i, [vp, i]),
+        "lb_gather": (i, [vp, vp, i]),
+        "lb_peek": (i, [vp, i, vp]),
+        "lb_invariants": (i, [vp, vp]),
+        "lb_sync": (i, [vp]),
+        "lb_profile_enable": (i, [vp, i]), "lb_profile_reset": (i, [vp]),
+        "lb_profile_read": (i, [vp, p(lb_kprof), i, p(i)]),
+        "lb_launch_count": (ctypes.c_int64, [vp]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = L
+    return L
+
+
+def _check(status: int):
+    if status != 0:
+        raise LBError(status, lib().lb_last_error().decode())
+
+
+def _dptr(a: np.ndarray):
+    assert a.dtype == np.float64 and a.flags.c_contiguous
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+# ---- host-only helpers (no GPU needed) ----------------------------------------
+
+def constants():
+    """(c[37,2] int, w[37], a, T0) as the library uses them."""
+    c = np.zeros(2 * Q, dtype=np.int32)
+    w = np.zeros(Q)
+    a = ctypes.c_double()
+    t0 = ctypes.c_double()
+    _check(lib().lb_constants(c.ctypes.data_as(ctypes.c_void_p), _dptr(w), ctypes.byref(a), ctypes.byref(t0)))
+    return c.reshape(Q, 2).astype(np.int64), w, a.value, t0.value
+
+
+def t0() -> float:
+    return constants()[3]
+
+
+def kwall(t_wall: float) -> np.ndarray:
+    K = np.zeros(Q)
+    _check(lib().lb_kwall(float(t_wall), _dptr(K)))
+    return K
+
+
+def make_params(lx_total, ly, tau=0.8, dt=1.0, t_bottom=None, t_top=None, bc_y="thermal",
+                mode="fused", overlap=False) -> lb_params:
+    T0 = t0()
+    return lb_params(int(lx_total), int(ly), float(tau), float(dt),
+                     float(1.05 * T0 if t_bottom is None else t_bottom),
+                     float(0.95 * T0 if t_top is None else t_top),
+                     BC[bc_y] if isinstance(bc_y, str) else int(bc_y),
+                     MODE[mode] if isinstance(mode, str) else int(mode), int(bool(overlap)))
+
+
+def query_layout(params: lb_params, rank: int = 0, nranks: int = 1) -> lb_layout:
+    L = lb_layout()
+    _check(lib().lb_query_layout(ctypes.byref(params), rank, nranks, ctypes.byref(L)))
+    return L
+
+
+def nccl_unique_id() -> bytes:
+    buf = (ctypes.c_ubyte * 128)()
+    _check(lib().lb_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+# ---- the lattice context --------------------------------------------------------
+
+class Lattice:
+    """One rank's X-slab of the D2Q37 lattice on the current CUDA device.
+
+    Buffers A/B are torch float64 tensors owned by this object (the library
+    borrows them, include/lb.h "Ownership")."""
+
+    def __init__(self, lx_total, ly, tau=0.8, dt=1.0, t_bottom=None, t_top=None, bc_y="thermal",
+                 mode="fused", overlap=False, rank=0, nranks=1, nccl_id: bytes | None = None,
+                 device=None, stream=None):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_1703_00186_b200 needs a CUDA device (no CPU fallback)")
+        self.params = make_params(lx_total, ly, tau, dt, t_bottom, t_top, bc_y, mode, overlap)
+        self.layout = query_layout(self.params, rank, nranks)
+        self.rank, self.nranks = rank, nranks
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.stream = torch.cuda.current_stream(self.device) if stream is None else stream
+        n = int(self.layout.elems)
+        self.bufs = [torch.empty(n, dtype=torch.float64, device=self.device) for _ in range(2)]
+        self._id = (ctypes.c_ubyte * 128).from_buffer_copy(nccl_id) if nccl_id is not None else None
+        dist = lb_dist(rank, nranks, ctypes.cast(self._id, ctypes.c_void_p) if self._id is not None else None)
+        ctx = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            _check(lib().lb_init(ctypes.byref(self.params), ctypes.byref(dist),
+                                 ctypes.c_void_p(self.bufs[0].data_ptr()),
+                                 ctypes.c_void_p(self.bufs[1].data_ptr()),
+                                 ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(ctx)))
+        self._ctx = ctx
+
+    # lifetime
+    def close(self):
+        if getattr(self, "_ctx", None):
+            lib().lb_destroy(self._ctx)
+            self._ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def lx(self):
+        return self.layout.lx
+
+    @property
+    def ly(self):
+        return self.layout.ly
+
+    @property
+    def sites(self):
+        return int(self.layout.sites)
+
+    # state in
+    def init_macro(self, rho, ux, uy, T):
+        import torch
+        arrs = [rho, ux, uy, T]
+        if all(isinstance(a, torch.Tensor) and a.is_cuda for a in arrs):
+            arrs = [a.contiguous() for a in arrs]
+            for a in arrs:
+                assert a.dtype == torch.float64 and a.numel() == self.sites
+            _check(lib().lb_init_macro(self._ctx, *[ctypes.c_void_p(a.data_ptr()) for a in arrs], 1))
+            self._keep = arrs
+        else:
+            arrs = [np.ascontiguousarray(np.asarray(a, dtype=np.float64)) for a in arrs]
+            for a in arrs:
+                assert a.size == self.sites
+            _check(lib().lb_init_macro(self._ctx, *[_dptr(a) for a in arrs], 0))
+            self.sync()
+
+    def set_state(self, canon):
+        import torch
+        if isinstance(canon, torch.Tensor) and canon.is_cuda:
+            assert canon.dtype == torch.float64 and canon.numel() == Q * self.sites
+            canon = canon.contiguous()
+            _check(lib().lb_set_state(self._ctx, ctypes.c_void_p(canon.data_ptr()), 1))
+            self._keep = [canon]
+        else:
+            a = np.ascontiguousarray(np.asarray(canon, dtype=np.float64))
+            assert a.size == Q * self.sites
+            _check(lib().lb_set_state(self._ctx, _dptr(a), 0))
+            self.sync()
+
+    # the hot path
+    def exchange(self):
+        _check(lib().lb_exchange(self._ctx))
+
+    def propagate(self):
+        _check(lib().lb_propagate(self._ctx))
+
+    def bc(self):
+        _check(lib().lb_bc(self._ctx))
+
+    def collide(self):
+        _check(lib().lb_collide(self._ctx))
+
+    def step(self, n: int = 1):
+        _check(lib().lb_step(self._ctx, int(n)))
+
+    def sync(self):
+        _check(lib().lb_sync(self._ctx))
+
+    # results
+    def gather(self, root: int = 0, out: np.ndarray | None = None):
+        """Canonical global state [37][lx_total][ly] on root (None elsewhere)."""
+        shape = (Q, self.params.lx_total, self.ly)
+        if self.rank == root:
+            if out is None:
+                out = np.empty(shape)
+            assert out.shape == shape and out.dtype == np.float64 and out.flags.c_contiguous
+            _check(lib().lb_gather(self._ctx, _dptr(out), root))
+            return out
+        _check(lib().lb_gather(self._ctx, None, root))
+        return None
+
+    def peek(self, which: int = 0) -> np.ndarray:
+        out = np.empty((Q, self.lx, self.ly))
+        _check(lib().lb_peek(self._ctx, which, _dptr(out)))
+        return out
+
+    def invariants(self) -> np.ndarray:
+        """[sum rho, sum jx, sum jy, sum E, min rho] (raises LBError on LB_ENONPHYS)."""
+        out = np.zeros(5)
+        _check(lib().lb_invariants(self._ctx, _dptr(out)))
+        return out
+
+    # instrumentation
+    def profile(self, enable: bool = True):
+        _check(lib().lb_profile_enable(self._ctx, int(enable)))
+
+    def profile_reset(self):
+        _check(lib().lb_profile_reset(self._ctx))
+
+    def profile_read(self) -> dict:
+        recs = (lb_kprof * 64)()
+        n = ctypes.c_int()
+        _check(lib().lb_profile_read(self._ctx, recs, 64, ctypes.byref(n)))
+        return {recs[i].name.decode(): {"launches": recs[i].launches, "total_ms": recs[i].total_ms,
+                                        "units": recs[i].units} for i in range(min(n.value, 64))}
+
+    def launch_count(self) -> int:
+        return int(lib().lb_launch_count(self._ctx))

@@ -1,0 +1,240 @@
+"""Parity of the CUDA path (through the C ABI) with the CPU oracle.
+
+Bars (BASELINE.json north_star): pbc / propagate / bc bit-exact; collide and
+full steps within 1e-12 max relative error in fp64 (G17: max over physical
+(l, x, y) of |f - f_ref| / |f_ref|, with f_ref > 1e-12 asserted).
+
+Inputs: lbgen macro fields (no LB arithmetic) fed to each side's own
+equilibrium (``init_macro``), or lbgen random population fields for the pure
+data-movement kernels.  For the isolated collide test the input state is built
+by the oracle on the host and uploaded to both sides (oracle -> GPU only;
+nothing flows from the GPU to the oracle).
+"""
+import numpy as np
+import pytest
+
+import lbgen
+import oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+Q = 37
+TOL = 1e-12
+BCN = {"thermal": oracle.WALL_THERMAL, "adiabatic": oracle.WALL_ADIABATIC, "periodic": oracle.PERIODIC}
+
+
+@pytest.fixture(scope="module")
+def lb():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1703_00186_b200 as m
+    m.lib()
+    return m
+
+
+def pair(lb, lx, ly, bc="thermal", mode="fused", overlap=False, tau=0.8, tb=None, tt=None):
+    T0 = oracle.t0()
+    tb = 1.05 * T0 if tb is None else tb
+    tt = 0.95 * T0 if tt is None else tt
+    g = lb.Lattice(lx, ly, tau=tau, t_bottom=tb, t_top=tt, bc_y=bc, mode=mode, overlap=overlap)
+    o = oracle.Lattice(lx, ly, tau=tau, t_bottom=tb, t_top=tt, bc_y=BCN[bc])
+    return g, o
+
+
+def max_rel(a, ref):
+    assert a.shape == ref.shape
+    assert np.all(np.abs(ref) > 1e-12), "G17: reference values must stay away from 0"
+    return float(np.max(np.abs(a - ref) / np.abs(ref)))
+
+
+def oracle_state(lx, ly, seed=3, noise=0.01):
+    """A realistic post-collision-like state built by the oracle: f_eq of random
+    near-equilibrium macro fields times (1 + noise) (test infrastructure)."""
+    o = oracle.Lattice(lx, ly, bc_y=oracle.PERIODIC)
+    o.init_macro(*lbgen.perturbed_macro(lx, ly, oracle.t0(), seed=seed))
+    st = o.get_state(0)
+    return st * (1.0 + noise * lbgen.uniform_noise(st.shape, seed=seed + 1))
+
+
+# ------------------------------------------------------------------ state I/O
+
+def test_set_state_gather_peek_roundtrip(lb):
+    g = lb.Lattice(37, 45)
+    st = lbgen.random_field(Q, 37, 45, seed=1)
+    g.set_state(st)
+    assert np.array_equal(g.gather(), st)
+    assert np.array_equal(g.peek(0), st)
+    dev = torch.from_numpy(st).cuda()
+    g.set_state(dev)
+    assert np.array_equal(g.gather(), st)
+
+
+@pytest.mark.parametrize("macro", ["rt", "perturbed"])
+def test_init_macro_equilibrium_parity(lb, macro):
+    lx, ly = 64, 32
+    fields = lbgen.rt_macro(lx, ly, oracle.t0()) if macro == "rt" else lbgen.perturbed_macro(lx, ly, oracle.t0())
+    g, o = pair(lb, lx, ly)
+    g.init_macro(*fields)
+    o.init_macro(*fields)
+    assert max_rel(g.gather(), o.get_state(0)) < 1e-13
+    # device-resident macro input path
+    g.init_macro(*[torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in fields])
+    assert max_rel(g.gather(), o.get_state(0)) < 1e-13
+
+
+# ------------------------------------------------------------------ per-kernel, identical inputs
+
+@pytest.mark.parametrize("bc", ["thermal", "adiabatic", "periodic"])
+@pytest.mark.parametrize("shape", [(64, 32), (3, 6), (7, 131), (130, 37)])
+def test_pbc_propagate_bc_bit_exact(lb, bc, shape):
+    lx, ly = shape
+    if bc != "periodic" and ly < 6:
+        pytest.skip()
+    g, o = pair(lb, lx, ly, bc=bc, mode="split")
+    st = lbgen.random_field(Q, lx, ly, seed=lx + ly)
+    g.set_state(st)
+    o.set_state(st)
+    g.exchange()
+    g.propagate()
+    o.pbc()
+    o.propagate()
+    assert np.array_equal(g.peek(1), o.get_state(1)), "propagate (raw pull) not bit-exact"
+    g.bc()
+    o.bc()
+    assert np.array_equal(g.peek(1), o.get_state(1)), "bc not bit-exact"
+
+
+@pytest.mark.parametrize("tau", [0.8, 1.0, 0.5, 2.0])
+def test_collide_parity(lb, tau):
+    lx, ly = 40, 33
+    st = oracle_state(lx, ly, seed=int(tau * 10))
+    g, o = pair(lb, lx, ly, bc="periodic", mode="split", tau=tau)
+    g.set_state(st)
+    o.set_state(st)
+    # periodic: exchange + propagate are bit-exact (tested above), bc is a no-op
+    g.exchange(); g.propagate(); g.bc(); g.collide()
+    o.step(1)
+    assert max_rel(g.gather(), o.get_state(0)) < TOL
+
+
+# ------------------------------------------------------------------ trajectories (config #1)
+
+@pytest.mark.parametrize("mode,overlap", [("split", False), ("fused", False), ("fused", True)])
+@pytest.mark.parametrize("bc", ["thermal", "adiabatic", "periodic"])
+def test_trajectory_64x32_10_steps(lb, mode, overlap, bc):
+    """Config #1: 64x32, RT init on each side, 10 steps, compared after every step."""
+    lx, ly = 64, 32
+    g, o = pair(lb, lx, ly, bc=bc, mode=mode, overlap=overlap)
+    fields = lbgen.rt_macro(lx, ly, oracle.t0())
+    g.init_macro(*fields)
+    o.init_macro(*fields)
+    for k in range(10):
+        g.step(1)
+        o.step(1)
+        err = max_rel(g.gather(), o.get_state(0))
+        assert err < TOL, (k, err)
+    inv_g = g.invariants()
+    inv_o = o.invariants(0)
+    assert abs(inv_g[0] - inv_o[0]) / inv_o[0] < 1e-13
+    assert np.allclose(inv_g[1:4], inv_o[1:4], rtol=1e-12, atol=1e-13 * inv_o[0])
+
+
+@pytest.mark.parametrize("shape,tau,bc", [((3, 6), 0.8, "thermal"), ((7, 131), 0.5, "thermal"),
+                                          ((130, 37), 1.0, "adiabatic"), ((12, 3), 0.6, "periodic"),
+                                          ((33, 200), 2.0, "thermal")])
+def test_trajectory_edge_shapes(lb, shape, tau, bc):
+    lx, ly = shape
+    g, o = pair(lb, lx, ly, bc=bc, tau=tau)
+    fields = lbgen.perturbed_macro(lx, ly, oracle.t0(), seed=lx * ly)
+    g.init_macro(*fields)
+    o.init_macro(*fields)
+    g.step(5)
+    o.step(5)
+    assert max_rel(g.gather(), o.get_state(0)) < TOL
+
+
+# ------------------------------------------------------------------ internal consistency (bitwise)
+
+@pytest.mark.parametrize("bc", ["thermal", "periodic"])
+def test_split_fused_overlap_bit_identical(lb, bc):
+    lx, ly = 70, 129
+    st = oracle_state(lx, ly, seed=9)
+    outs = []
+    for mode, ov in [("split", False), ("fused", False), ("fused", True)]:
+        g = lb.Lattice(lx, ly, bc_y=bc, mode=mode, overlap=ov)
+        g.set_state(st)
+        g.step(7)
+        outs.append(g.gather())
+    assert np.array_equal(outs[0], outs[1])
+    assert np.array_equal(outs[1], outs[2])
+
+
+def test_uniform_wall_equilibrium_fixed_point(lb):
+    Tw = 0.98 * oracle.t0()
+    lx, ly = 32, 64
+    g = lb.Lattice(lx, ly, t_bottom=Tw, t_top=Tw)
+    ones = np.ones((lx, ly))
+    g.init_macro(1.02 * ones, 0 * ones, 0 * ones, Tw * ones)
+    st0 = g.gather()
+    g.step(100)
+    assert np.abs(g.gather() - st0).max() / st0.max() < 1e-12
+
+
+# ------------------------------------------------------------------ invariants / errors
+
+def test_invariants_and_nonphysical_detection(lb):
+    lx, ly = 48, 40
+    g, o = pair(lb, lx, ly)
+    fields = lbgen.perturbed_macro(lx, ly, oracle.t0(), seed=4)
+    g.init_macro(*fields)
+    o.init_macro(*fields)
+    inv = g.invariants()
+    ref = o.invariants(0)
+    assert abs(inv[0] - ref[0]) / ref[0] < 1e-13
+    assert np.allclose(inv[1:4], ref[1:4], rtol=1e-12, atol=1e-13 * ref[0])
+    assert 0.9 < inv[4] < 1.1
+    st = g.gather()
+    st[5, 3, 7] = np.nan
+    g.set_state(st)
+    with pytest.raises(lb.LBError) as ei:
+        g.invariants()
+    assert ei.value.status == 5
+    st[5, 3, 7] = -20.0
+    g.set_state(st)
+    with pytest.raises(lb.LBError) as ei:
+        g.invariants()
+    assert ei.value.status == 5
+
+
+def test_call_order_errors(lb):
+    g = lb.Lattice(16, 16, mode="split")
+    with pytest.raises(lb.LBError) as ei:
+        g.bc()
+    assert ei.value.status == 2
+    g.propagate()
+    with pytest.raises(lb.LBError) as ei:
+        g.gather()
+    assert ei.value.status == 2
+    g.bc()
+    g.collide()
+    g.gather()
+
+
+# ------------------------------------------------------------------ full size (config #2)
+
+@pytest.mark.parametrize("overlap", [False, True])
+def test_full_size_1920x2048_one_step(lb, overlap):
+    """Config #2 lattice in the launch configuration bench.py times (fused)."""
+    lx, ly = 1920, 2048
+    fields = lbgen.rt_macro(lx, ly, oracle.t0())
+    g = lb.Lattice(lx, ly, mode="fused", overlap=overlap)
+    g.init_macro(*fields)
+    g.step(2)
+    got = g.gather()
+    del g
+    o = oracle.Lattice(lx, ly)
+    o.init_macro(*fields)
+    o.step(2)
+    ref = o.get_state(0)
+    assert max_rel(got, ref) < TOL
