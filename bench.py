@@ -107,29 +107,31 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- oracle leg
 
-def oracle_throughput(lx_total: int, ly: int, budget_s: float, steps: int | None = None):
-    """The CPU oracle, as it stands, on a bounded sample of the workload: the
-    first w columns of the same RT lattice (all ly rows), w sized so the run
-    takes about budget_s.  Returns (MLUPS, cores, sample description)."""
+def oracle_throughput(lx_total: int, ly: int, budget_s: float):
+    """The CPU oracle, as it stands, on a bounded sample of the workload: full
+    time steps of the same RT lattice (the whole lattice if one step fits the
+    budget, else its first w columns with all ly rows), as many steps as fit
+    in about budget_s.  Returns (MLUPS, cores, sample description)."""
     import lbgen
     import oracle
     T0 = oracle.t0()
-    probe_w = min(lx_total, 16)
+    probe_w = min(lx_total, 32)
     o = oracle.Lattice(probe_w, ly)
     o.init_macro(*lbgen.rt_macro(lx_total, ly, T0, lx=probe_w))
+    o.step(1)
     t = time.perf_counter()
     o.step(1)
     per_site = (time.perf_counter() - t) / (probe_w * ly)
-    nsteps = steps if steps is not None else 3
-    w = int(max(3, min(lx_total, budget_s / (per_site * ly * nsteps))))
+    w = int(max(3, min(lx_total, budget_s / (per_site * ly))))
+    nsteps = int(max(1, min(50, budget_s / (per_site * w * ly))))
     o = oracle.Lattice(w, ly)
     o.init_macro(*lbgen.rt_macro(lx_total, ly, T0, lx=w))
     t = time.perf_counter()
     o.step(nsteps)
     dt = time.perf_counter() - t
     mlups = w * ly * nsteps / dt / 1e6
-    sample = (f"oracle lbref (C, -O2 -ffp-contract=off, OpenMP over ix) full steps on columns 0..{w - 1} "
-              f"of the {lx_total}x{ly} RT workload, {nsteps} steps, {dt:.1f} s")
+    sample = (f"oracle lbref (C, -O2 -ffp-contract=off, OpenMP over ix) {nsteps} full step(s) on "
+              f"columns 0..{w - 1} (all {ly} rows) of the {lx_total}x{ly} RT workload, {dt:.1f} s")
     return mlups, oracle.threads(), sample, dt, w, nsteps
 
 

@@ -115,6 +115,26 @@ typedef struct lb_layout {
   int64_t sites;         /* lx * ly physical sites of this rank                */
 } lb_layout;
 
+/* The ring exchange of one rank (§8a1, §8e), as lb_exchange / lb_step issue
+ * it: offsets are element offsets into the rank's A buffer (internal layout),
+ * each message is `count` contiguous doubles (3 full columns).  The four
+ * transfers are posted in this order inside one NCCL group: receive the left
+ * halo from `left`, receive the right halo from `right`, send the right border
+ * to `right`, send the left border to `left` — so for N = 2 (left == right)
+ * the k-th send of a rank matches the k-th receive of its peer.  Bulk and
+ * border column ranges (internal column indices) are those of the overlapped
+ * schedule: the bulk reads no halo column. */
+typedef struct lb_xplan {
+  int left, right;              /* ring neighbours                 */
+  int64_t count;                /* doubles per message = 3 * 37 * nyp          */
+  int64_t recv_left_off;        /* columns [0, 3): left halo                   */
+  int64_t recv_right_off;       /* columns [lx+3, lx+6): right halo            */
+  int64_t send_right_off;       /* columns [lx, lx+3): -> right's left halo    */
+  int64_t send_left_off;        /* columns [3, 6): -> left's right halo        */
+  int bulk_x0, bulk_x1;         /* bulk columns [bulk_x0, bulk_x1)             */
+  int border_x0, border_x1, border_x2, border_x3; /* [x0,x1) U [x2,x3)        */
+} lb_xplan;
+
 typedef struct lb_ctx lb_ctx;
 
 /* Per-kernel timing record (see lb_profile_enable). */
@@ -141,6 +161,9 @@ int lb_constants(int* c, double* w, double* a, double* t0);
 /* Wall constants K_wall,l(T_wall) (App. B, canonical expression tree G16)
  * exactly as uploaded by lb_init: K[37]. */
 int lb_kwall(double t_wall, double* K);
+
+/* Fill *out with the exchange plan of (rank, nranks) for p (host only). */
+int lb_exchange_plan(const lb_params* p, int rank, int nranks, lb_xplan* out);
 
 /* ncclGetUniqueId into out[128] (rank 0 calls it; broadcast it to the others). */
 int lb_nccl_unique_id(unsigned char* out);

@@ -75,6 +75,7 @@ struct ProfEntry {
 struct lb_ctx {
   lb_params p{};
   lb_layout L{};
+  lb_xplan X{};
   Geo g{};
   int rank = 0, nranks = 1, left = 0, right = 0;
   double *A = nullptr, *B = nullptr;
@@ -193,10 +194,26 @@ void fill_layout(const lb_params* p, int rank, int nranks, lb_layout* L) {
   L->sites = (int64_t)L->lx * L->ly;
 }
 
+void fill_plan(const lb_layout& L, int rank, int nranks, lb_xplan* x) {
+  x->left = (rank - 1 + nranks) % nranks;
+  x->right = (rank + 1) % nranks;
+  x->count = 3 * L.col_stride;
+  x->recv_left_off = 0;
+  x->recv_right_off = (int64_t)(L.lx + 3) * L.col_stride;
+  x->send_right_off = (int64_t)L.lx * L.col_stride;
+  x->send_left_off = (int64_t)3 * L.col_stride;
+  x->bulk_x0 = LB_HALO + 3;
+  x->bulk_x1 = std::max(LB_HALO + 3, LB_HALO + L.lx - 3);
+  x->border_x0 = LB_HALO;
+  x->border_x1 = LB_HALO + 3;
+  x->border_x2 = LB_HALO + L.lx - 3;
+  x->border_x3 = LB_HALO + L.lx;
+}
+
 Cols all_cols(const lb_ctx* c) { return Cols{LB_HALO, LB_HALO + c->g.lx, 0, 0}; }
-Cols bulk_cols(const lb_ctx* c) { return Cols{LB_HALO + 3, LB_HALO + c->g.lx - 3, 0, 0}; }
+Cols bulk_cols(const lb_ctx* c) { return Cols{c->X.bulk_x0, c->X.bulk_x1, 0, 0}; }
 Cols border_cols(const lb_ctx* c) {
-  return Cols{LB_HALO, LB_HALO + 3, LB_HALO + c->g.lx - 3, LB_HALO + c->g.lx};
+  return Cols{c->X.border_x0, c->X.border_x1, c->X.border_x2, c->X.border_x3};
 }
 
 // ---- exchange (§8a1) -------------------------------------------------------
@@ -212,16 +229,13 @@ int exchange_on(lb_ctx* c, cudaStream_t s) {
       return lbk::launch_pbc_wrap(g, c->A, c->p.bc_y, s);
     });
   }
-  const size_t n = (size_t)3 * g.cs;
-  double* halo_l = c->A;
-  double* halo_r = c->A + (int64_t)(g.lx + 3) * g.cs;
-  double* bord_l = c->A + (int64_t)3 * g.cs;
-  double* bord_r = c->A + (int64_t)g.lx * g.cs;
+  const lb_xplan& x = c->X;
+  const size_t n = (size_t)x.count;
   NC(ncclGroupStart());
-  NC(ncclRecv(halo_l, n, ncclDouble, c->left, c->comm, s));
-  NC(ncclRecv(halo_r, n, ncclDouble, c->right, c->comm, s));
-  NC(ncclSend(bord_r, n, ncclDouble, c->right, c->comm, s));
-  NC(ncclSend(bord_l, n, ncclDouble, c->left, c->comm, s));
+  NC(ncclRecv(c->A + x.recv_left_off, n, ncclDouble, x.left, c->comm, s));
+  NC(ncclRecv(c->A + x.recv_right_off, n, ncclDouble, x.right, c->comm, s));
+  NC(ncclSend(c->A + x.send_right_off, n, ncclDouble, x.right, c->comm, s));
+  NC(ncclSend(c->A + x.send_left_off, n, ncclDouble, x.left, c->comm, s));
   NC(ncclGroupEnd());
   if (c->p.bc_y == LB_PERIODIC)
     TRY(launch(c, "k_ywrap", s, 0, [&] { return lbk::launch_ywrap(g, c->A, s); }));
@@ -305,6 +319,15 @@ int lb_query_layout(const lb_params* p, int rank, int nranks, lb_layout* out) {
   return LB_OK;
 }
 
+int lb_exchange_plan(const lb_params* p, int rank, int nranks, lb_xplan* out) {
+  TRY(validate(p, rank, nranks));
+  if (!out) return fail(LB_EINVAL, "out is NULL");
+  lb_layout L;
+  fill_layout(p, rank, nranks, &L);
+  fill_plan(L, rank, nranks, out);
+  return LB_OK;
+}
+
 int lb_constants(int* c, double* w, double* a, double* t0) {
   for (int l = 0; l < lbd::Q; ++l) {
     if (c) {
@@ -347,6 +370,7 @@ int lb_init(const lb_params* p, const lb_dist* d, double* f_a, double* f_b, void
   c->p = *p;
   fill_layout(p, rank, nranks, &c->L);
   c->g = make_geo(c->L);
+  fill_plan(c->L, rank, nranks, &c->X);
   c->rank = rank;
   c->nranks = nranks;
   c->left = (rank - 1 + nranks) % nranks;

@@ -24,7 +24,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 SO_PATH = os.path.join(_HERE, "liblb_d2q37.so")
 
 # every symbol include/lb.h declares
-EXPORTS = ["lb_query_layout", "lb_constants", "lb_kwall", "lb_nccl_unique_id", "lb_last_error",
+EXPORTS = ["lb_query_layout", "lb_exchange_plan", "lb_constants", "lb_kwall", "lb_nccl_unique_id", "lb_last_error",
            "lb_strerror", "lb_init", "lb_destroy", "lb_get_layout", "lb_set_stream", "lb_init_macro",
            "lb_set_state", "lb_exchange", "lb_propagate", "lb_bc", "lb_collide", "lb_step",
            "lb_gather", "lb_peek", "lb_invariants", "lb_sync", "lb_profile_enable",
@@ -53,6 +53,15 @@ class lb_layout(ctypes.Structure):
                 ("elems", ctypes.c_int64), ("bytes", ctypes.c_int64), ("sites", ctypes.c_int64)]
 
 
+class lb_xplan(ctypes.Structure):
+    _fields_ = [("left", ctypes.c_int), ("right", ctypes.c_int), ("count", ctypes.c_int64),
+                ("recv_left_off", ctypes.c_int64), ("recv_right_off", ctypes.c_int64),
+                ("send_right_off", ctypes.c_int64), ("send_left_off", ctypes.c_int64),
+                ("bulk_x0", ctypes.c_int), ("bulk_x1", ctypes.c_int),
+                ("border_x0", ctypes.c_int), ("border_x1", ctypes.c_int),
+                ("border_x2", ctypes.c_int), ("border_x3", ctypes.c_int)]
+
+
 class lb_kprof(ctypes.Structure):
     _fields_ = [("name", ctypes.c_char * 32), ("launches", ctypes.c_int64),
                 ("total_ms", ctypes.c_double), ("units", ctypes.c_int64)]
@@ -75,6 +84,7 @@ def lib():
     sig = {
         "lb_query_layout": (i, [p(lb_params), i, i, p(lb_layout)]),
         "lb_constants": (i, [vp, vp, vp, vp]),
+        "lb_exchange_plan": (i, [p(lb_params), i, i, p(lb_xplan)]),
         "lb_kwall": (i, [d, vp]),
         "lb_nccl_unique_id": (i, [vp]),
         "lb_last_error": (ctypes.c_char_p, []),
@@ -149,6 +159,12 @@ def query_layout(params: lb_params, rank: int = 0, nranks: int = 1) -> lb_layout
     L = lb_layout()
     _check(lib().lb_query_layout(ctypes.byref(params), rank, nranks, ctypes.byref(L)))
     return L
+
+
+def exchange_plan(params: lb_params, rank: int = 0, nranks: int = 1) -> lb_xplan:
+    X = lb_xplan()
+    _check(lib().lb_exchange_plan(ctypes.byref(params), rank, nranks, ctypes.byref(X)))
+    return X
 
 
 def nccl_unique_id() -> bytes:
