@@ -123,7 +123,7 @@ def oracle_throughput(lx_total: int, ly: int, budget_s: float):
     o.step(1)
     per_site = (time.perf_counter() - t) / (probe_w * ly)
     w = int(max(3, min(lx_total, budget_s / (per_site * ly))))
-    nsteps = int(max(1, min(50, budget_s / (per_site * w * ly))))
+    nsteps = int(max(1, min(1000, budget_s / (per_site * w * ly))))
     o = oracle.Lattice(w, ly)
     o.init_macro(*lbgen.rt_macro(lx_total, ly, T0, lx=w))
     t = time.perf_counter()

@@ -99,7 +99,10 @@ typedef struct lb_params {
 typedef struct lb_dist {
   int rank;              /* this process' slab, 0..nranks-1                    */
   int nranks;            /* ring size N; lx_total % N == 0                     */
-  const unsigned char* nccl_id; /* 128-byte ncclUniqueId from rank 0, or NULL if N == 1 */
+  const unsigned char* nccl_id; /* 128-byte ncclUniqueId from rank 0.  Required if
+                            N > 1.  At N == 1, NULL selects the local wrap kernel;
+                            non-NULL runs the exchange through NCCL as a 1-rank ring
+                            (self send/recv) — the N > 1 transport on one GPU. */
 } lb_dist;
 
 typedef struct lb_layout {

@@ -86,6 +86,7 @@ struct lb_ctx {
   double* d_part = nullptr;   // invariants partials (+5 result doubles)
   double* h_pin = nullptr;    // pinned 8 doubles for results
   int phase = 0;              // 0 = step boundary, 1 = after propagate, 2 = after bc
+  bool halo_fresh = false;    // A's x-halo columns already hold the wrap of A (N = 1)
   double omega = 1.0;
   int64_t launches = 0;
   // instrumentation
@@ -224,7 +225,7 @@ Cols border_cols(const lb_ctx* c) {
 // receive of the peer in the right halo.
 int exchange_on(lb_ctx* c, cudaStream_t s) {
   const Geo& g = c->g;
-  if (c->nranks == 1) {
+  if (!c->comm) {
     return launch(c, "k_pbc_wrap", s, 6LL * g.ly, [&] {
       return lbk::launch_pbc_wrap(g, c->A, c->p.bc_y, s);
     });
@@ -242,21 +243,31 @@ int exchange_on(lb_ctx* c, cudaStream_t s) {
   return LB_OK;
 }
 
-int fused(lb_ctx* c, Cols cols) {
+int fused(lb_ctx* c, Cols cols, int wrap = 0) {
   return launch(c, "k_step_fused", c->s, (int64_t)cols.count() * c->g.ly, [&] {
-    return lbk::launch_step_fused(c->g, c->A, c->B, c->p.bc_y, c->omega, cols, c->s);
+    return lbk::launch_step_fused(c->g, c->A, c->B, c->p.bc_y, c->omega, cols, wrap, c->s);
   });
 }
 
 int step_once(lb_ctx* c) {
-  const bool overlap = c->p.overlap && c->p.mode == LB_MODE_FUSED && c->g.lx >= 6 &&
-                       !(c->p.bc_y == LB_PERIODIC && c->nranks > 1);
   if (c->p.mode == LB_MODE_SPLIT) {
     TRY(lb_exchange(c));
     TRY(lb_propagate(c));
     TRY(lb_bc(c));
     return lb_collide(c);
   }
+  // N = 1 without NCCL, walls: the fused kernel writes the next step's halo
+  // columns itself (one launch per step); a separate wrap only when A's halo
+  // is stale (after lb_set_state / lb_init_macro / a split step).
+  if (!c->comm && c->p.bc_y != LB_PERIODIC) {
+    if (!c->halo_fresh) TRY(exchange_on(c, c->s));
+    TRY(fused(c, all_cols(c), 1));
+    std::swap(c->A, c->B);
+    c->halo_fresh = true;
+    return LB_OK;
+  }
+  const bool overlap = c->p.overlap && c->g.lx >= 6 && !(c->p.bc_y == LB_PERIODIC && c->comm != nullptr);
+  c->halo_fresh = false;
   if (!overlap) {
     TRY(lb_exchange(c));
     TRY(fused(c, all_cols(c)));
@@ -402,7 +413,7 @@ int lb_init(const lb_params* p, const lb_dist* d, double* f_a, double* f_b, void
   kwall(p->t_top, kt);
   if (lbk::upload_kwall(kb, kt, c->s) != cudaSuccess)
     return bail(fail(LB_ECUDA, "constant upload failed"));
-  if (nranks > 1) {
+  if (nranks > 1 || (d && d->nccl_id)) {
     ncclUniqueId id;
     std::memcpy(&id, d->nccl_id, 128);
     ncclResult_t r = ncclCommInitRank(&c->comm, nranks, id, rank);
@@ -460,6 +471,7 @@ int lb_init_macro(lb_ctx* c, const double* rho, const double* ux, const double* 
       dev[k] = dst;
     }
   }
+  c->halo_fresh = false;
   TRY(launch(c, "k_init_macro", c->s, n, [&] {
     return lbk::launch_init_macro(c->g, c->A, dev[0], dev[1], dev[2], dev[3], c->s);
   }));
@@ -476,6 +488,7 @@ int lb_set_state(lb_ctx* c, const double* canon, int on_device) {
     CU(cudaMemcpyAsync(c->B, canon, n * sizeof(double), cudaMemcpyHostToDevice, c->s));
     src = c->B;
   }
+  c->halo_fresh = false;
   TRY(launch(c, "k_canon_to_internal", c->s, c->L.sites, [&] {
     return lbk::launch_canon_to_internal(c->g, src, c->A, c->s);
   }));
@@ -485,7 +498,11 @@ int lb_set_state(lb_ctx* c, const double* canon, int on_device) {
 
 int lb_exchange(lb_ctx* c) {
   TRY(check_boundary(c, "lb_exchange"));
-  if (c->nranks == 1) return exchange_on(c, c->s);
+  if (!c->comm) {
+    TRY(exchange_on(c, c->s));
+    c->halo_fresh = true;
+    return LB_OK;
+  }
   CU(cudaEventRecord(c->ev_ready, c->s));
   CU(cudaStreamWaitEvent(c->s_comm, c->ev_ready, 0));
   TRY(exchange_on(c, c->s_comm));
@@ -523,6 +540,7 @@ int lb_collide(lb_ctx* c) {
   }));
   std::swap(c->A, c->B);
   c->phase = 0;
+  c->halo_fresh = false;
   return LB_OK;
 }
 
@@ -596,7 +614,7 @@ int lb_invariants(lb_ctx* c, double* out) {
   TRY(launch(c, "k_invariants", c->s, c->L.sites, [&] {
     return lbk::launch_invariants(c->g, c->A, c->d_part, res, c->s);
   }));
-  if (c->nranks > 1) {
+  if (c->comm) {
     NC(ncclGroupStart());
     NC(ncclAllReduce(res, res, 4, ncclDouble, ncclSum, c->comm, c->s));
     NC(ncclAllReduce(res + 4, res + 4, 1, ncclDouble, ncclMin, c->comm, c->s));

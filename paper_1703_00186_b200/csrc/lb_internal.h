@@ -33,7 +33,7 @@ cudaError_t launch_propagate(const Geo& g, const double* A, double* B, cudaStrea
 cudaError_t launch_bc(const Geo& g, const double* A, double* B, int bc, cudaStream_t s);
 cudaError_t launch_collide(const Geo& g, double* B, double omega, cudaStream_t s);
 cudaError_t launch_step_fused(const Geo& g, const double* A, double* B, int bc, double omega,
-                              Cols cols, cudaStream_t s);
+                              Cols cols, int wrap, cudaStream_t s);
 cudaError_t launch_init_macro(const Geo& g, double* A, const double* rho, const double* ux,
                               const double* uy, const double* T, cudaStream_t s);
 cudaError_t launch_canon_to_internal(const Geo& g, const double* canon, double* A, cudaStream_t s);

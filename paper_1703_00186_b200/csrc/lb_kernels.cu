@@ -115,6 +115,20 @@ __device__ __forceinline__ void gather(const double* __restrict__ A, const Geo& 
   }
 }
 
+// Same pull without MIRROR, with the 37 loads as ordered volatile coherent
+// ld.global: ptxas may not sink them below the possibly-aliasing stores (it
+// does with .nc), so all 37 loads are in flight before the first store (pure
+// copy kernel: maximum memory-level parallelism per thread).
+__device__ __forceinline__ void gather_ordered(const double* __restrict__ A, const Geo& g, int ix,
+                                               int y, double (&f)[Q]) {
+  const double* b = A + (int64_t)ix * g.cs + g.y0 + y;
+#pragma unroll
+  for (int l = 0; l < Q; ++l) {
+    const double* p = b + ((int64_t)l * g.nyp - (int64_t)CX(l) * g.cs - CY(l));
+    asm volatile("ld.global.f64 %0, [%1];" : "=d"(f[l]) : "l"(p));
+  }
+}
+
 __device__ __forceinline__ void store_site(double* __restrict__ B, const Geo& g, int ix, int y,
                                            const double (&f)[Q]) {
   double* p = B + (int64_t)ix * g.cs + g.y0 + y;
@@ -131,7 +145,10 @@ __global__ void __launch_bounds__(TPB) k_propagate(const double* __restrict__ A,
   const int ix = H + blockIdx.y;
   if (y >= g.ly) return;
   double f[Q];
-  gather<false>(A, g, ix, y, f);
+  // all 37 loads in flight before the first store (the compiler would
+  // otherwise pair load/store and keep only a few loads outstanding)
+  gather_ordered(A, g, ix, y, f);
+  asm volatile("" ::: "memory");
   store_site(B, g, ix, y, f);
 }
 
@@ -211,10 +228,14 @@ cudaError_t launch_collide(const Geo& g, double* B, double omega, cudaStream_t s
 // gather (+mirror) -> thermal wall -> collide -> store, A -> B in one pass:
 // 296 B read + 296 B written per site.  Warps whose 32 rows are all at least
 // 3 rows from both walls take the mirror-free gather (warp-uniform branch).
+// wrap != 0 (N = 1 without NCCL): the blocks of the 3+3 border columns also
+// store their result into B's halo columns (pbc of the NEXT step done in the
+// producing kernel: left halo [0,3) <- [lx, lx+3), right halo [lx+3, lx+6) <-
+// [3, 6)), so the step needs no separate wrap launch.
 template <int BC>
 __global__ void __launch_bounds__(TPB) k_step_fused(const double* __restrict__ A,
                                                     double* __restrict__ B, Geo g, Cols cols,
-                                                    double omega, double one_m_omega) {
+                                                    double omega, double one_m_omega, int wrap) {
   const int y = blockIdx.x * TPB + threadIdx.x;
   const int na = cols.xa1 - cols.xa0;
   const int ix = (int)blockIdx.y < na ? cols.xa0 + (int)blockIdx.y : cols.xb0 + ((int)blockIdx.y - na);
@@ -234,18 +255,22 @@ __global__ void __launch_bounds__(TPB) k_step_fused(const double* __restrict__ A
   }
   collide_site(f, omega, one_m_omega);
   store_site(B, g, ix, y, f);
+  if (wrap) {
+    if (ix < 2 * H) store_site(B, g, ix + g.lx, y, f);
+    if (ix >= g.lx) store_site(B, g, ix - g.lx, y, f);
+  }
 }
 
 cudaError_t launch_step_fused(const Geo& g, const double* A, double* B, int bc, double omega,
-                              Cols cols, cudaStream_t s) {
+                              Cols cols, int wrap, cudaStream_t s) {
   const int n = cols.count();
   if (n <= 0) return cudaSuccess;
   dim3 grid((g.ly + TPB - 1) / TPB, n);
   const double om1 = 1.0 - omega;
   switch (bc) {
-    case BC_THERMAL: k_step_fused<BC_THERMAL><<<grid, TPB, 0, s>>>(A, B, g, cols, omega, om1); break;
-    case BC_ADIABATIC: k_step_fused<BC_ADIABATIC><<<grid, TPB, 0, s>>>(A, B, g, cols, omega, om1); break;
-    default: k_step_fused<BC_PERIODIC><<<grid, TPB, 0, s>>>(A, B, g, cols, omega, om1); break;
+    case BC_THERMAL: k_step_fused<BC_THERMAL><<<grid, TPB, 0, s>>>(A, B, g, cols, omega, om1, wrap); break;
+    case BC_ADIABATIC: k_step_fused<BC_ADIABATIC><<<grid, TPB, 0, s>>>(A, B, g, cols, omega, om1, wrap); break;
+    default: k_step_fused<BC_PERIODIC><<<grid, TPB, 0, s>>>(A, B, g, cols, omega, om1, wrap); break;
   }
   return cudaGetLastError();
 }

@@ -238,3 +238,28 @@ def test_full_size_1920x2048_one_step(lb, overlap):
     o.step(2)
     ref = o.get_state(0)
     assert max_rel(got, ref) < TOL
+
+
+# ------------------------------------------------------------------ NCCL transport on one GPU
+
+@pytest.mark.parametrize("bc,mode,overlap", [("thermal", "fused", True), ("thermal", "fused", False),
+                                             ("thermal", "split", False), ("periodic", "fused", True),
+                                             ("adiabatic", "fused", True)])
+def test_nccl_self_ring_equals_local_wrap(lb, bc, mode, overlap):
+    """N = 1 with an NCCL communicator: the exchange runs the N > 1 code path
+    (grouped ncclSend/ncclRecv of the contiguous 3-column blocks on the comm
+    stream, bulk || exchange, borders after the event) as a 1-rank ring; it
+    must be bit-identical to the local wrap, and invariants go through
+    ncclAllReduce."""
+    lx, ly = 40, 70
+    st = oracle_state(lx, ly, seed=31)
+    ref = lb.Lattice(lx, ly, bc_y=bc, mode=mode)
+    ref.set_state(st)
+    ref.step(6)
+    want = ref.gather()
+    g = lb.Lattice(lx, ly, bc_y=bc, mode=mode, overlap=overlap, nccl_id=lb.nccl_unique_id())
+    g.set_state(st)
+    g.step(6)
+    assert np.array_equal(g.gather(), want)
+    assert np.allclose(g.invariants(), ref.invariants(), rtol=1e-15, atol=0)
+    g.close()
