@@ -19,6 +19,7 @@ import numpy as np
 Q = 37
 HALO = 3
 WALL_THERMAL, WALL_ADIABATIC, PERIODIC = 0, 1, 2
+BGK, REGULARIZED = 0, 1
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "liblbref.so")
@@ -54,7 +55,8 @@ def lib():
             "lbref_refl": (i, [i]), "lbref_opp": (i, [i]),
             "lbref_macro": (v, [p, p]), "lbref_feq": (v, [d, d, d, d, p]),
             "lbref_kwall": (v, [d, p]), "lbref_collide_site": (v, [p, d]),
-            "lbref_init": (p, [i, i, d, d, d, d, i]), "lbref_free": (v, [p]),
+            "lbref_project": (v, [p, p]), "lbref_collide_site_reg": (v, [p, d]),
+            "lbref_init": (p, [i, i, d, d, d, d, i, i]), "lbref_free": (v, [p]),
             "lbref_nx": (i, [p]), "lbref_ny": (i, [p]), "lbref_buffer": (dp, [p, i]),
             "lbref_set_state": (v, [p, p]), "lbref_get_state": (v, [p, i, p]),
             "lbref_init_macro": (v, [p, p, p, p, p]),
@@ -133,17 +135,33 @@ def collide_site(f, omega) -> np.ndarray:
     return f
 
 
+def project(f) -> np.ndarray:
+    """Hermite projection onto orders <= 4 (reading G6)."""
+    f = np.ascontiguousarray(f, dtype=np.float64)
+    out = np.zeros(Q)
+    lib().lbref_project(_ptr(f), _ptr(out))
+    return out
+
+
+def collide_site_reg(f, omega) -> np.ndarray:
+    """Regularised collide: f_eq + (1 - omega)(P f - f_eq)."""
+    f = np.array(f, dtype=np.float64)
+    lib().lbref_collide_site_reg(_ptr(f), float(omega))
+    return f
+
+
 # ---- lattice stepper --------------------------------------------------------
 
 class Lattice:
     """One slab (N=1) of the canonical layout [37][Lx+6][Ly+6]."""
 
-    def __init__(self, lx, ly, tau=0.8, dt=1.0, t_bottom=None, t_top=None, bc_y=WALL_THERMAL):
+    def __init__(self, lx, ly, tau=0.8, dt=1.0, t_bottom=None, t_top=None, bc_y=WALL_THERMAL,
+                 collision=BGK):
         T0 = t0()
         t_bottom = 1.05 * T0 if t_bottom is None else t_bottom
         t_top = 0.95 * T0 if t_top is None else t_top
         self.lx, self.ly = lx, ly
-        self._h = lib().lbref_init(lx, ly, tau, dt, t_bottom, t_top, bc_y)
+        self._h = lib().lbref_init(lx, ly, tau, dt, t_bottom, t_top, bc_y, collision)
         if not self._h:
             raise ValueError("lbref_init rejected the parameters")
         self.nx = lib().lbref_nx(self._h)

@@ -167,10 +167,79 @@ void lbref_collide_site(double f[Q], double omega)
     for (int l = 0; l < Q; ++l) f[l] = f[l] - omega * (f[l] - feq[l]);
 }
 
+/* Tensor Hermite polynomial H^(n)_{i1..in}(xi), n <= 4, in D = 2 (reading G6):
+ *   H0 = 1, H1_i = xi_i, H2_ij = xi_i xi_j - d_ij,
+ *   H3_ijk = xi_i xi_j xi_k - (xi_i d_jk + xi_j d_ik + xi_k d_ij),
+ *   H4_ijkl = xi_i xi_j xi_k xi_l - (xi_i xi_j d_kl + xi_i xi_k d_jl + xi_i xi_l d_jk
+ *             + xi_j xi_k d_il + xi_j xi_l d_ik + xi_k xi_l d_ij)
+ *             + (d_ij d_kl + d_ik d_jl + d_il d_jk). */
+static double kd(int i, int j) { return i == j ? 1.0 : 0.0; }
+
+static double hermite(int n, const int* t, const double* xi)
+{
+    switch (n) {
+    case 0: return 1.0;
+    case 1: return xi[t[0]];
+    case 2: return xi[t[0]] * xi[t[1]] - kd(t[0], t[1]);
+    case 3: {
+        const int i = t[0], j = t[1], k = t[2];
+        return xi[i] * xi[j] * xi[k] - (xi[i] * kd(j, k) + xi[j] * kd(i, k) + xi[k] * kd(i, j));
+    }
+    default: {
+        const int i = t[0], j = t[1], k = t[2], l = t[3];
+        return xi[i] * xi[j] * xi[k] * xi[l]
+             - (xi[i] * xi[j] * kd(k, l) + xi[i] * xi[k] * kd(j, l) + xi[i] * xi[l] * kd(j, k)
+                + xi[j] * xi[k] * kd(i, l) + xi[j] * xi[l] * kd(i, k) + xi[k] * xi[l] * kd(i, j))
+             + (kd(i, j) * kd(k, l) + kd(i, k) * kd(j, l) + kd(i, l) * kd(j, k));
+    }
+    }
+}
+
+/* Hermite projection ("systematic projection onto a basis of
+ * Hermite polynomials"; reading G6): a^(n) = sum_l f_l H^(n)(xi_l) for every
+ * index tuple, then out_l = w_l sum_{n=0}^{4} (1/n!) sum_tuples a^(n) H^(n)(xi_l),
+ * the full tensor contraction over all 2^n index tuples. */
+void lbref_project(const double f[Q], double out[Q])
+{
+    int c[Q][2];
+    double w[Q];
+    lbref_velocities(c);
+    lbref_weights(w);
+    double xi[Q][2];
+    for (int l = 0; l < Q; ++l) {
+        xi[l][0] = A_SCALE * c[l][0];
+        xi[l][1] = A_SCALE * c[l][1];
+        out[l] = 0.0;
+    }
+    double fact = 1.0;
+    for (int n = 0; n <= 4; ++n) {
+        if (n > 0) fact *= n;
+        const int ntup = 1 << n;
+        for (int m = 0; m < ntup; ++m) {
+            int t[4];
+            for (int b = 0; b < n; ++b) t[b] = (m >> b) & 1;
+            double a = 0.0;
+            for (int l = 0; l < Q; ++l) a += f[l] * hermite(n, t, xi[l]);
+            for (int l = 0; l < Q; ++l) out[l] += w[l] * (a / fact) * hermite(n, t, xi[l]);
+        }
+    }
+}
+
+/* Regularised collide: relax in the Hermite space of
+ * orders <= 4 and drop the rest: f <- f_eq + (1 - omega)(P f - f_eq). */
+void lbref_collide_site_reg(double f[Q], double omega)
+{
+    double m[4], feq[Q], pf[Q];
+    lbref_macro(f, m);
+    lbref_feq(m[0], m[1], m[2], m[3], feq);
+    lbref_project(f, pf);
+    for (int l = 0; l < Q; ++l) f[l] = feq[l] + (1.0 - omega) * (pf[l] - feq[l]);
+}
+
 /* ------------------------------------------------------------------------ */
 
 struct lbref {
-    int lx, ly, nx, ny, bc_y;
+    int lx, ly, nx, ny, bc_y, collision;
     double omega, t_bottom, t_top;
     double *a, *b;            /* canonical [Q][NX][NY] */
     int c[Q][2];
@@ -181,11 +250,12 @@ struct lbref {
 #define IDX(s, l, ix, iy) (((size_t)(l) * (s)->nx + (size_t)(ix)) * (s)->ny + (size_t)(iy))
 
 lbref* lbref_init(int lx, int ly, double tau, double dt,
-                  double t_bottom, double t_top, int bc_y)
+                  double t_bottom, double t_top, int bc_y, int collision)
 {
     if (lx < 3 || ly < 3) return NULL;
     if (bc_y != LBREF_PERIODIC && ly < 6) return NULL;
     if (bc_y < 0 || bc_y > 2) return NULL;
+    if (collision != LBREF_BGK && collision != LBREF_REGULARIZED) return NULL;
     if (!(tau > 0.0) || !(dt > 0.0)) return NULL;
     double om = dt / tau;
     if (!(om > 0.0 && om <= 2.0)) return NULL;
@@ -197,6 +267,7 @@ lbref* lbref_init(int lx, int ly, double tau, double dt,
     s->nx = lx + 2 * HX;
     s->ny = ly + 2 * HY;
     s->bc_y = bc_y;
+    s->collision = collision;
     s->omega = om;
     s->t_bottom = t_bottom;
     s->t_top = t_top;
@@ -332,7 +403,10 @@ void lbref_collide(lbref* s)
         for (int iy = HY; iy < HY + s->ly; ++iy) {
             double f[Q];
             for (int l = 0; l < Q; ++l) f[l] = s->b[IDX(s, l, ix, iy)];
-            lbref_collide_site(f, s->omega);
+            if (s->collision == LBREF_REGULARIZED)
+                lbref_collide_site_reg(f, s->omega);
+            else
+                lbref_collide_site(f, s->omega);
             for (int l = 0; l < Q; ++l) s->b[IDX(s, l, ix, iy)] = f[l];
         }
 }

@@ -47,11 +47,17 @@ void   lbref_feq(double rho, double ux, double uy, double T, double out[LBREF_Q]
 void   lbref_kwall(double t_wall, double K[LBREF_Q]);
 /* Eq. 1 collide of one site in place, omega = dt/tau (O7)                   */
 void   lbref_collide_site(double f[LBREF_Q], double omega);
+/* Hermite projection onto orders <= 4 (reading G6):
+ * out_l = w_l sum_{n<=4} (1/n!) a^(n) : H^(n)(xi_l),  a^(n) = sum_l f_l H^(n)(xi_l)  */
+void   lbref_project(const double f[LBREF_Q], double out[LBREF_Q]);
+/* Regularised collide in place: f <- f_eq + (1 - omega)(P f - f_eq)          */
+void   lbref_collide_site_reg(double f[LBREF_Q], double omega);
 
 /* ---- lattice stepper --------------------------------------------------- */
-/* Returns NULL on invalid parameters (Lx<1, Ly<6, dt/tau not in (0,2], T<=0) */
+enum { LBREF_BGK = 0, LBREF_REGULARIZED = 1 };
+/* Returns NULL on invalid parameters (Lx<3, Ly<6, dt/tau not in (0,2], T<=0) */
 lbref* lbref_init(int lx, int ly, double tau, double dt,
-                  double t_bottom, double t_top, int bc_y);
+                  double t_bottom, double t_top, int bc_y, int collision);
 void   lbref_free(lbref*);
 int    lbref_nx(const lbref*);
 int    lbref_ny(const lbref*);

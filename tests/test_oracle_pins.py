@@ -405,3 +405,76 @@ def test_walled_rt_step_conserves_mass_and_stays_physical():
     m = L.invariants(0)[0]
     assert abs(m - m0) / m0 < 1e-13
     assert L.get_state(0).min() > 0
+
+
+# ---------------------------------------------------------------- Hermite projection (NEXT 1, G6)
+
+def _monomials():
+    """V[l, k] = cx^p cy^q for the 15 exponents p + q <= 4 (lattice units)."""
+    c = oracle.velocities().astype(float)
+    exps = [(p, q) for n in range(5) for p in range(n + 1) for q in [n - p]]
+    return np.stack([c[:, 0] ** p * c[:, 1] ** q for p, q in exps], axis=1), exps
+
+
+def test_projection_is_weighted_least_squares():
+    """P f = W V (V^T W V)^-1 V^T f: the orthogonal projection onto {w_l p(c_l): deg p <= 4}
+    under <g, h> = sum g h / w, computed in the monomial basis by linear algebra —
+    independent of the oracle's Hermite-tensor contraction."""
+    V, _ = _monomials()
+    w = oracle.weights()
+    for seed in range(4):
+        f = lbgen.random_field(Q, 1, 1, seed=40 + seed).reshape(Q)
+        beta = np.linalg.solve(V.T @ (w[:, None] * V), V.T @ f)
+        ref = w * (V @ beta)
+        # rounding: 37-term sums of Hermite values up to |xi|^4 ~ 170
+        assert np.allclose(oracle.project(f), ref, rtol=0, atol=2e-13 * np.abs(ref).max())
+
+
+def test_projection_properties():
+    V, _ = _monomials()
+    w = oracle.weights()
+    f = _near_eq_f(5) * (1 + 0.2 * lbgen.uniform_noise(Q, seed=77))
+    pf = oracle.project(f)
+    assert np.allclose(oracle.project(pf), pf, rtol=0, atol=1e-15)          # idempotent
+    assert np.allclose(V.T @ pf, V.T @ f, rtol=1e-13, atol=1e-15)           # moments p+q<=4 kept
+    r = f - pf
+    assert np.abs(V.T @ r).max() < 1e-14                                    # residual orthogonal
+    assert np.abs(r).max() > 1e-5                                           # and nonzero
+    feq = oracle.feq(1.1, 0.03, -0.02, 0.75)
+    assert np.allclose(oracle.project(feq), feq, rtol=1e-13, atol=0)        # f_eq in the space
+    assert np.allclose(oracle.project(w), w, rtol=1e-14, atol=0)
+
+
+@pytest.mark.parametrize("omega", [1.25, 1.0, 0.6, 2.0])
+def test_regularized_collide_conservation_and_limits(omega):
+    c = oracle.velocities().astype(float)
+    c2 = (c ** 2).sum(axis=1)
+    f = _near_eq_f(11)
+    g = oracle.collide_site_reg(f, omega)
+    assert abs(g.sum() - f.sum()) < 1e-14 * f.sum()
+    assert np.allclose(c.T @ g, c.T @ f, rtol=0, atol=1e-15)
+    assert abs(c2 @ g - c2 @ f) < 1e-14 * (c2 @ f)
+    m = oracle.macro(f)
+    feq = oracle.feq(*m)
+    if omega == 1.0:
+        assert np.allclose(g, feq, rtol=1e-13, atol=0)
+    assert np.allclose(oracle.collide_site_reg(feq, omega), feq, rtol=1e-13, atol=0)
+    # linear in omega around f_eq: g = f_eq + (1 - omega)(P f - f_eq)
+    pf = oracle.project(f)
+    assert np.allclose(g, feq + (1 - omega) * (pf - feq), rtol=1e-13, atol=1e-18)
+
+
+def test_regularized_equals_bgk_inside_hermite_space():
+    """If f already lies in the order-<=4 Hermite space, regularised == BGK."""
+    f = oracle.project(_near_eq_f(13))
+    assert np.allclose(oracle.collide_site_reg(f, 1.25), oracle.collide_site(f, 1.25), rtol=1e-12, atol=0)
+
+
+def test_regularized_periodic_step_conserves_invariants():
+    lx, ly = 24, 20
+    L = oracle.Lattice(lx, ly, bc_y=oracle.PERIODIC, collision=oracle.REGULARIZED)
+    L.init_macro(*lbgen.perturbed_macro(lx, ly, oracle.t0(), seed=22))
+    inv0 = L.invariants(0)
+    L.step(50)
+    inv = L.invariants(0)
+    assert np.abs(inv - inv0).max() / inv0[0] < 1e-13
