@@ -179,6 +179,42 @@ def workload_config(cfg_name, lx_total, ly, world, mode):
             "tau": 0.8, "bc_y": "thermal", "init": "isobaric RT (lbgen, seed 1703)"}
 
 
+def kernel_passes(lb, lx_total, ly, fields, hbm_peak, fp64_peak, ncu, nsteps=10):
+    """Per-kernel CUDA-event times of split BGK, fused regularised and split
+    regularised steps on the same workload (library instrumentation)."""
+    kern = {}
+    for mode, coll in (("split", "bgk"), ("fused", "regularized"), ("split", "regularized")):
+        g = lb.Lattice(lx_total, ly, mode=mode, collision=coll)
+        g.init_macro(*fields)
+        g.step(3)
+        g.profile(True)
+        g.profile_reset()
+        g.step(nsteps)
+        sp = g.profile_read()
+        g.close()
+        for k, v in sp.items():
+            if k in kern:
+                continue
+            avg = v["total_ms"] / max(1, v["launches"])
+            e = {"avg_ms": avg, "launches": v["launches"]}
+            if k in ("k_propagate", "k_collide", "k_collide_reg", "k_step_fused_reg"):
+                per = BYTES_PER_SITE * v["units"] / v["launches"]
+                e["gbs"] = per / (avg * 1e-3) / 1e9
+                e["hbm_frac"] = e["gbs"] / hbm_peak
+                e["mlups"] = v["units"] / v["launches"] / (avg * 1e-3) / 1e6
+            if k in ("k_collide", "k_collide_reg", "k_step_fused_reg"):
+                fl = ncu.get("kernels", {}).get(k, {}).get("flops_per_site")
+                if fl and fp64_peak:
+                    tf = fl * e["mlups"] * 1e6 / 1e12
+                    e.update({"flops_per_site_ncu": fl, "fp64_tflops": tf, "fp64_frac": tf / fp64_peak,
+                              "fp64_peak_tflops": fp64_peak})
+                e["paper_convention_6500_flop_tflops"] = 6500 * e["mlups"] * 1e6 / 1e12
+            kern[k] = e
+        step_ms = sum(v["total_ms"] for v in sp.values()) / nsteps
+        kern[f"{mode}_{coll}_step_mlups"] = lx_total * ly / (step_ms * 1e-3) / 1e6
+    return kern
+
+
 # ----------------------------------------------------------------------------- our leg
 
 def main():
@@ -302,44 +338,14 @@ def main():
     line["config"]["overlap"] = overlap
 
     if not args.no_extras:
-        # ---- per-kernel split pass (propagate GB/s, collide FP64 % of peak)
-        gs = lb.Lattice(lx_total, ly, mode="split", rank=rank, nranks=world, nccl_id=None) if world == 1 else None
-        if gs is not None:
-            del g
-            torch.cuda.empty_cache()
-            gs.init_macro(*fields)
-            gs.step(3)
-            gs.profile(True)
-            gs.profile_reset()
-            gs.step(10)
-            sp = gs.profile_read()
-            kern = {}
-            for k, v in sp.items():
-                avg = v["total_ms"] / max(1, v["launches"])
-                kern[k] = {"avg_ms": avg, "launches": v["launches"]}
-                if k in ("k_propagate", "k_collide"):
-                    per = BYTES_PER_SITE * v["units"] / v["launches"]
-                    kern[k]["gbs"] = per / (avg * 1e-3) / 1e9
-                    kern[k]["hbm_frac"] = kern[k]["gbs"] / hbm_peak
-                if k == "k_collide":
-                    kern[k]["mlups"] = v["units"] / v["launches"] / (avg * 1e-3) / 1e6
-                    fl = ncu.get("kernels", {}).get("k_collide", {}).get("flops_per_site")
-                    if fl and fp64_peak:
-                        tf = fl * kern[k]["mlups"] * 1e6 / 1e12
-                        kern[k].update({"flops_per_site_ncu": fl, "fp64_tflops": tf,
-                                        "fp64_frac": tf / fp64_peak, "fp64_peak_tflops": fp64_peak})
-                    kern[k]["paper_convention_6500_flop_tflops"] = 6500 * kern[k]["mlups"] * 1e6 / 1e12
-            split_ms = sum(v["total_ms"] for v in sp.values()) / 10
-            kern["split_step_mlups"] = lx_total * ly / (split_ms * 1e-3) / 1e6
-            line["kernels"] = kern
-            g = gs
-        # ---- e2e through the C ABI with pinned host buffers
+        # ---- e2e through the C ABI with pinned host buffers (same fused path)
         state_bytes = 37 * g.sites * 8
         host_in = torch.empty(37 * g.sites, dtype=torch.float64).pin_memory()
         host_out = torch.empty((37, lx_total, ly), dtype=torch.float64).pin_memory() if rank == 0 else None
-        st0 = g.gather() if world == 1 else None
-        if st0 is not None:
-            host_in.numpy()[:] = st0.reshape(-1)
+        g.init_macro(*fields)
+        st0 = g.peek(0)
+        host_in.numpy()[:] = st0.reshape(-1)
+        del st0
         k_e2e = max(10, min(args.steps, 100))
         barrier()
         torch.cuda.synchronize()
@@ -348,14 +354,21 @@ def main():
         for _ in range(k_e2e):
             g.step(1)
             g.invariants()
-        out = g.gather(out=host_out.numpy() if host_out is not None else None)
+        g.gather(out=host_out.numpy() if host_out is not None else None)
         e2e_s = max_over_ranks(time.perf_counter() - t)
         line["e2e"] = {"value": round(sites_all * k_e2e / e2e_s / 1e6, 2), "unit": "MLUPS",
                        "h2d_bytes_per_step": state_bytes / k_e2e,
                        "d2h_bytes_per_step": (state_bytes + 5 * 8 * k_e2e) / k_e2e,
-                       "steps": k_e2e,
+                       "steps": k_e2e, "mode": args.mode,
                        "timed": "lb_set_state(pinned host) + K x (lb_step(1) + lb_invariants -> host) + lb_gather(pinned host)"}
-        del out
+        del host_in, host_out
+        # ---- per-kernel passes (N = 1): split BGK (propagate GB/s, collide FP64 %),
+        #      fused and split regularised collide (NEXT 1)
+        if world == 1:
+            g.close()
+            del g
+            torch.cuda.empty_cache()
+            line["kernels"] = kernel_passes(lb, lx_total, ly, fields, hbm_peak, fp64_peak, ncu)
         # ---- CPU oracle baseline (rank 0, N = 1 only)
         if world == 1 and rank == 0:
             mlups, cores, sample, dt, w, ns = oracle_throughput(lx_total, ly,

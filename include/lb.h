@@ -79,6 +79,12 @@ enum lb_bc_y {
   LB_PERIODIC = 2        /* no bc; y-halo rows wrapped by pbc (test geometry)    */
 };
 
+enum lb_collision {
+  LB_COLLIDE_BGK = 0,         /* Eq. 1 BGK relaxation to f_eq (App. B)          */
+  LB_COLLIDE_REGULARIZED = 1  /* Hermite-projected (orders <= 4):
+                                 f <- f_eq + (1 - dt/tau)(P f - f_eq) (NEXT 1)   */
+};
+
 enum lb_mode {
   LB_MODE_FUSED = 0,     /* one pull kernel: propagate+bc+collide, A -> B     */
   LB_MODE_SPLIT = 1      /* propagate, bc, collide as separate kernels        */
@@ -94,6 +100,7 @@ typedef struct lb_params {
   int bc_y;              /* enum lb_bc_y                                       */
   int mode;              /* enum lb_mode                                       */
   int overlap;           /* 1: exchange || bulk, then borders     */
+  int collision;         /* enum lb_collision                                 */
 } lb_params;
 
 typedef struct lb_dist {

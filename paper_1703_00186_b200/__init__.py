@@ -3,5 +3,5 @@
 The product is the C-ABI CUDA library ``liblb_d2q37.so`` (include/lb.h,
 sources in ``csrc/``); ``lb`` is its thin Python binding.
 """
-from .lb import (BC, MODE, Q, HALO, LBError, Lattice, constants, kwall, make_params,  # noqa: F401
+from .lb import (BC, MODE, COLLISION, Q, HALO, LBError, Lattice, constants, kwall, make_params,  # noqa: F401
                  nccl_unique_id, query_layout, exchange_plan, t0, lib, SO_PATH, EXPORTS)

@@ -64,6 +64,47 @@ void kwall(double t_wall, double* K) {
   }
 }
 
+// Packed block inverse of the Gram matrix G_ab = sum_l w_l c_l^(alpha_a + alpha_b)
+// of the 15 monomials |alpha| <= 4 (regularised collide, lb_kernels.cu).
+// Each parity block is inverted by Gauss-Jordan with partial pivoting in long
+// double.  Returns false if a block is singular.
+bool gram_inverse(double* out) {
+  for (int g = 0; g < 4; ++g) {
+    const int first = lbd::GBLK_FIRST(g), n = lbd::GBLK_SIZE(g), off = lbd::GBLK_OFF(g);
+    long double a[6][12];
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) {
+        long double s = 0.0L;
+        const int p = lbd::MP(first + i) + lbd::MP(first + j), q = lbd::MQ(first + i) + lbd::MQ(first + j);
+        for (int l = 0; l < lbd::Q; ++l) {
+          long double t = host_weight(l);
+          for (int k = 0; k < p; ++k) t *= lbd::CX(l);
+          for (int k = 0; k < q; ++k) t *= lbd::CY(l);
+          s += t;
+        }
+        a[i][j] = s;
+        a[i][n + j] = (i == j) ? 1.0L : 0.0L;
+      }
+    for (int col = 0; col < n; ++col) {
+      int piv = col;
+      for (int r = col + 1; r < n; ++r)
+        if (fabsl(a[r][col]) > fabsl(a[piv][col])) piv = r;
+      if (fabsl(a[piv][col]) < 1e-30L) return false;
+      for (int k = 0; k < 2 * n; ++k) std::swap(a[col][k], a[piv][k]);
+      const long double d = a[col][col];
+      for (int k = 0; k < 2 * n; ++k) a[col][k] /= d;
+      for (int r = 0; r < n; ++r)
+        if (r != col) {
+          const long double m = a[r][col];
+          for (int k = 0; k < 2 * n; ++k) a[r][k] -= m * a[col][k];
+        }
+    }
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) out[off + i * n + j] = (double)a[i][n + j];
+  }
+  return true;
+}
+
 struct ProfEntry {
   int kernel;
   cudaEvent_t e0, e1;
@@ -172,6 +213,7 @@ int validate(const lb_params* p, int rank, int nranks) {
   if (p->bc_y < 0 || p->bc_y > 2) return fail(LB_EINVAL, "bad bc_y");
   if (p->ly < (p->bc_y == LB_PERIODIC ? 3 : 6)) return fail(LB_EINVAL, "ly = %d too small", p->ly);
   if (p->mode < 0 || p->mode > 1) return fail(LB_EINVAL, "bad mode");
+  if (p->collision < 0 || p->collision > 1) return fail(LB_EINVAL, "bad collision");
   if (!(p->tau > 0.0) || !(p->dt > 0.0)) return fail(LB_EINVAL, "tau and dt must be > 0");
   const double om = p->dt / p->tau;
   if (!(om > 0.0 && om <= 2.0)) return fail(LB_EINVAL, "dt/tau must be in (0, 2]");
@@ -244,8 +286,8 @@ int exchange_on(lb_ctx* c, cudaStream_t s) {
 }
 
 int fused(lb_ctx* c, Cols cols, int wrap = 0) {
-  return launch(c, "k_step_fused", c->s, (int64_t)cols.count() * c->g.ly, [&] {
-    return lbk::launch_step_fused(c->g, c->A, c->B, c->p.bc_y, c->omega, cols, wrap, c->s);
+  return launch(c, c->p.collision ? "k_step_fused_reg" : "k_step_fused", c->s, (int64_t)cols.count() * c->g.ly, [&] {
+    return lbk::launch_step_fused(c->g, c->A, c->B, c->p.bc_y, c->p.collision, c->omega, cols, wrap, c->s);
   });
 }
 
@@ -266,7 +308,8 @@ int step_once(lb_ctx* c) {
     c->halo_fresh = true;
     return LB_OK;
   }
-  const bool overlap = c->p.overlap && c->g.lx >= 6 && !(c->p.bc_y == LB_PERIODIC && c->comm != nullptr);
+  // PERIODIC-Y: the y-halo wrap rewrites rows the bulk reads, so no overlap there
+  const bool overlap = c->p.overlap && c->g.lx >= 6 && c->p.bc_y != LB_PERIODIC;
   c->halo_fresh = false;
   if (!overlap) {
     TRY(lb_exchange(c));
@@ -413,6 +456,10 @@ int lb_init(const lb_params* p, const lb_dist* d, double* f_a, double* f_b, void
   kwall(p->t_top, kt);
   if (lbk::upload_kwall(kb, kt, c->s) != cudaSuccess)
     return bail(fail(LB_ECUDA, "constant upload failed"));
+  double ginv[lbd::NGINV];
+  if (!gram_inverse(ginv)) return bail(fail(LB_EINVAL, "singular Gram matrix"));
+  if (lbk::upload_ginv(ginv, c->s) != cudaSuccess)
+    return bail(fail(LB_ECUDA, "constant upload failed"));
   if (nranks > 1 || (d && d->nccl_id)) {
     ncclUniqueId id;
     std::memcpy(&id, d->nccl_id, 128);
@@ -535,8 +582,8 @@ int lb_collide(lb_ctx* c) {
   if (!c) return fail(LB_EINVAL, "ctx is NULL");
   if (c->phase != 2 && !(c->phase == 1 && c->p.bc_y == LB_PERIODIC))
     return fail(LB_ESTATE, "lb_collide must follow lb_bc");
-  TRY(launch(c, "k_collide", c->s, c->L.sites, [&] {
-    return lbk::launch_collide(c->g, c->B, c->omega, c->s);
+  TRY(launch(c, c->p.collision ? "k_collide_reg" : "k_collide", c->s, c->L.sites, [&] {
+    return lbk::launch_collide(c->g, c->B, c->omega, c->p.collision, c->s);
   }));
   std::swap(c->A, c->B);
   c->phase = 0;

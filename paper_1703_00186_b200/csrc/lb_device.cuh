@@ -63,6 +63,26 @@ LB_HD constexpr double SHELL_W(int s) {
 constexpr double A_SCALE = 1.19697977039307435897239;
 constexpr double A2 = A_SCALE * A_SCALE;
 
+// ---- regularised collide: moment index map ---------------------------------
+// The 15 monomials cx^p cy^q with p + q <= 4, grouped by the parity of (p, q):
+// the Gram matrix G_ab = sum_l w_l c^(alpha_a + alpha_b) is block-diagonal in
+// these groups (odd lattice moments vanish by symmetry).
+constexpr int NMOM = 15;
+LB_HD constexpr int MP(int k) {
+  constexpr int t[NMOM] = {0, 2, 0, 4, 2, 0, /*OE*/ 1, 3, 1, /*EO*/ 0, 0, 2, /*OO*/ 1, 3, 1};
+  return t[k];
+}
+LB_HD constexpr int MQ(int k) {
+  constexpr int t[NMOM] = {0, 0, 2, 0, 2, 4, /*OE*/ 0, 0, 2, /*EO*/ 1, 3, 1, /*OO*/ 1, 1, 3};
+  return t[k];
+}
+// block [first, first + size) of group g: EE (6), OE (3), EO (3), OO (3)
+LB_HD constexpr int GBLK_FIRST(int g) { return g == 0 ? 0 : 3 + 3 * g; }
+LB_HD constexpr int GBLK_SIZE(int g) { return g == 0 ? 6 : 3; }
+// offset of block g inside the packed inverse (36 + 9 + 9 + 9 = 63 doubles)
+LB_HD constexpr int GBLK_OFF(int g) { return g == 0 ? 0 : 36 + 9 * (g - 1); }
+constexpr int NGINV = 63;
+
 // ---- compile-time self checks of the table ---------------------------------
 constexpr bool table_ok() {
   int sx = 0, sy = 0, s2 = 0;

@@ -15,6 +15,7 @@ struct Geo {
 };
 
 enum BcKind { BC_THERMAL = 0, BC_ADIABATIC = 1, BC_PERIODIC = 2 };
+enum CollKind { COLL_BGK = 0, COLL_REGULARIZED = 1 };
 
 // Column ranges are in internal column indices (physical columns are
 // [3, 3+lx)).  A launch covers [xa0, xa1) U [xb0, xb1).
@@ -24,6 +25,8 @@ struct Cols {
 };
 
 cudaError_t upload_kwall(const double* k_bottom, const double* k_top, cudaStream_t s);
+// packed block inverse of the regularised-collide Gram matrix (lbd::NGINV doubles)
+cudaError_t upload_ginv(const double* ginv, cudaStream_t s);
 
 // N=1 periodic wrap of the x-halo columns (and y-halo rows when periodic).
 cudaError_t launch_pbc_wrap(const Geo& g, double* A, int bc, cudaStream_t s);
@@ -31,9 +34,9 @@ cudaError_t launch_pbc_wrap(const Geo& g, double* A, int bc, cudaStream_t s);
 cudaError_t launch_ywrap(const Geo& g, double* A, cudaStream_t s);
 cudaError_t launch_propagate(const Geo& g, const double* A, double* B, cudaStream_t s);
 cudaError_t launch_bc(const Geo& g, const double* A, double* B, int bc, cudaStream_t s);
-cudaError_t launch_collide(const Geo& g, double* B, double omega, cudaStream_t s);
-cudaError_t launch_step_fused(const Geo& g, const double* A, double* B, int bc, double omega,
-                              Cols cols, int wrap, cudaStream_t s);
+cudaError_t launch_collide(const Geo& g, double* B, double omega, int coll, cudaStream_t s);
+cudaError_t launch_step_fused(const Geo& g, const double* A, double* B, int bc, int coll,
+                              double omega, Cols cols, int wrap, cudaStream_t s);
 cudaError_t launch_init_macro(const Geo& g, double* A, const double* rho, const double* ux,
                               const double* uy, const double* T, cudaStream_t s);
 cudaError_t launch_canon_to_internal(const Geo& g, const double* canon, double* A, cudaStream_t s);

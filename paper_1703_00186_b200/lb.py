@@ -19,6 +19,7 @@ STATUS = {0: "LB_OK", 1: "LB_EINVAL", 2: "LB_ESTATE", 3: "LB_ECUDA", 4: "LB_ENCC
           5: "LB_ENONPHYS", 6: "LB_ENOMEM"}
 BC = {"thermal": 0, "adiabatic": 1, "periodic": 2}
 MODE = {"fused": 0, "split": 1}
+COLLISION = {"bgk": 0, "regularized": 1}
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 SO_PATH = os.path.join(_HERE, "liblb_d2q37.so")
@@ -40,7 +41,8 @@ class LBError(RuntimeError):
 class lb_params(ctypes.Structure):
     _fields_ = [("lx_total", ctypes.c_int), ("ly", ctypes.c_int), ("tau", ctypes.c_double),
                 ("dt", ctypes.c_double), ("t_bottom", ctypes.c_double), ("t_top", ctypes.c_double),
-                ("bc_y", ctypes.c_int), ("mode", ctypes.c_int), ("overlap", ctypes.c_int)]
+                ("bc_y", ctypes.c_int), ("mode", ctypes.c_int), ("overlap", ctypes.c_int),
+                ("collision", ctypes.c_int)]
 
 
 class lb_dist(ctypes.Structure):
@@ -146,13 +148,14 @@ def kwall(t_wall: float) -> np.ndarray:
 
 
 def make_params(lx_total, ly, tau=0.8, dt=1.0, t_bottom=None, t_top=None, bc_y="thermal",
-                mode="fused", overlap=False) -> lb_params:
+                mode="fused", overlap=False, collision="bgk") -> lb_params:
     T0 = t0()
     return lb_params(int(lx_total), int(ly), float(tau), float(dt),
                      float(1.05 * T0 if t_bottom is None else t_bottom),
                      float(0.95 * T0 if t_top is None else t_top),
                      BC[bc_y] if isinstance(bc_y, str) else int(bc_y),
-                     MODE[mode] if isinstance(mode, str) else int(mode), int(bool(overlap)))
+                     MODE[mode] if isinstance(mode, str) else int(mode), int(bool(overlap)),
+                     COLLISION[collision] if isinstance(collision, str) else int(collision))
 
 
 def query_layout(params: lb_params, rank: int = 0, nranks: int = 1) -> lb_layout:
@@ -183,11 +186,11 @@ class Lattice:
 
     def __init__(self, lx_total, ly, tau=0.8, dt=1.0, t_bottom=None, t_top=None, bc_y="thermal",
                  mode="fused", overlap=False, rank=0, nranks=1, nccl_id: bytes | None = None,
-                 device=None, stream=None):
+                 device=None, stream=None, collision="bgk"):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("paper_1703_00186_b200 needs a CUDA device (no CPU fallback)")
-        self.params = make_params(lx_total, ly, tau, dt, t_bottom, t_top, bc_y, mode, overlap)
+        self.params = make_params(lx_total, ly, tau, dt, t_bottom, t_top, bc_y, mode, overlap, collision)
         self.layout = query_layout(self.params, rank, nranks)
         self.rank, self.nranks = rank, nranks
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)

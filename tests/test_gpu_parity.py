@@ -263,3 +263,54 @@ def test_nccl_self_ring_equals_local_wrap(lb, bc, mode, overlap):
     assert np.array_equal(g.gather(), want)
     assert np.allclose(g.invariants(), ref.invariants(), rtol=1e-15, atol=0)
     g.close()
+
+
+# ------------------------------------------------------------------ regularised collide (NEXT 1)
+
+def reg_pair(lb, lx, ly, bc="thermal", mode="fused", tau=0.8):
+    T0 = oracle.t0()
+    g = lb.Lattice(lx, ly, tau=tau, bc_y=bc, mode=mode, collision="regularized")
+    o = oracle.Lattice(lx, ly, tau=tau, bc_y=BCN[bc], collision=oracle.REGULARIZED)
+    return g, o
+
+
+@pytest.mark.parametrize("tau", [0.8, 1.0, 0.55, 2.0])
+def test_regularized_collide_parity(lb, tau):
+    lx, ly = 40, 33
+    st = oracle_state(lx, ly, seed=int(tau * 100), noise=0.03)
+    g, o = reg_pair(lb, lx, ly, bc="periodic", mode="split", tau=tau)
+    g.set_state(st)
+    o.set_state(st)
+    g.exchange(); g.propagate(); g.bc(); g.collide()
+    o.step(1)
+    assert max_rel(g.gather(), o.get_state(0)) < TOL
+
+
+@pytest.mark.parametrize("mode", ["fused", "split"])
+@pytest.mark.parametrize("bc", ["thermal", "adiabatic"])
+def test_regularized_trajectory_64x32(lb, mode, bc):
+    lx, ly = 64, 32
+    g, o = reg_pair(lb, lx, ly, bc=bc, mode=mode)
+    fields = lbgen.rt_macro(lx, ly, oracle.t0())
+    g.init_macro(*fields)
+    o.init_macro(*fields)
+    for k in range(10):
+        g.step(1)
+        o.step(1)
+        assert max_rel(g.gather(), o.get_state(0)) < TOL, k
+
+
+def test_regularized_split_fused_bit_identical_and_256(lb):
+    lx, ly = 256, 256
+    fields = lbgen.perturbed_macro(lx, ly, oracle.t0(), seed=17)
+    outs = []
+    for mode in ("split", "fused"):
+        g = lb.Lattice(lx, ly, mode=mode, collision="regularized")
+        g.init_macro(*fields)
+        g.step(3)
+        outs.append(g.gather())
+    assert np.array_equal(outs[0], outs[1])
+    o = oracle.Lattice(lx, ly, collision=oracle.REGULARIZED)
+    o.init_macro(*fields)
+    o.step(3)
+    assert max_rel(outs[1], o.get_state(0)) < TOL

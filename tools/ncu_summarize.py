@@ -23,6 +23,10 @@ for r in rows:
     d = dict(zip(hdr, r))
     name = d["Kernel Name"].split("(")[0].replace("void ", "")
     base = name.split("<")[0]
+    targs = name[len(base):].strip("<>").replace(" ", "").split(",") if "<" in name else []
+    # collision kind is the last template argument of k_step_fused<BC, COLL> / k_collide<COLL>
+    if base in ("k_step_fused", "k_collide") and targs and targs[-1] == "1":
+        base += "_reg"
     try:
         v = float(d["Metric Value"].replace(",", ""))
     except ValueError:

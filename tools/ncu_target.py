@@ -1,6 +1,6 @@
-"""Small target for ncu: a few fused steps and a few split steps at 1920x2048.
+"""Small target for ncu: a few steps per (mode, collision) at 1920x2048.
 
-ncu --set full -k regex:'k_step_fused|k_propagate|k_collide|k_bc' ... python tools/ncu_target.py
+ncu ... python tools/ncu_target.py fused split fused:regularized split:regularized
 """
 import os
 import sys
@@ -13,8 +13,9 @@ import paper_1703_00186_b200 as lb  # noqa: E402
 
 lx, ly = int(os.environ.get("LB_LX", 1920)), int(os.environ.get("LB_LY", 2048))
 fields = lbgen.rt_macro(lx, ly, lb.t0())
-for mode in sys.argv[1:] or ["fused", "split"]:
-    g = lb.Lattice(lx, ly, mode=mode)
+for spec in sys.argv[1:] or ["fused", "split"]:
+    mode, _, coll = spec.partition(":")
+    g = lb.Lattice(lx, ly, mode=mode, collision=coll or "bgk")
     g.init_macro(*fields)
     g.step(3)
     g.sync()
