@@ -106,8 +106,9 @@ typedef struct lb_params {
 typedef struct lb_dist {
   int rank;              /* this process' slab, 0..nranks-1                    */
   int nranks;            /* ring size N; lx_total % N == 0                     */
-  const unsigned char* nccl_id; /* 128-byte ncclUniqueId from rank 0.  Required if
-                            N > 1.  At N == 1, NULL selects the local wrap kernel;
+  const unsigned char* nccl_id; /* 128-byte ncclUniqueId from rank 0.  N > 1 without
+                            it: only the peer-store exchange (lb_set_peers) is
+                            available.  At N == 1, NULL selects the local wrap kernel;
                             non-NULL runs the exchange through NCCL as a 1-rank ring
                             (self send/recv) — the N > 1 transport on one GPU. */
 } lb_dist;
@@ -144,6 +145,19 @@ typedef struct lb_xplan {
   int bulk_x0, bulk_x1;         /* bulk columns [bulk_x0, bulk_x1)             */
   int border_x0, border_x1, border_x2, border_x3; /* [x0,x1) U [x2,x3)        */
 } lb_xplan;
+
+/* Peer-store exchange ("exchange fused into the kernel"):
+ * device pointers, valid in this process (CUDA IPC mappings of the
+ * neighbours' buffers over NVLink, or plain pointers for contexts of one
+ * process), of the two neighbours' population buffers (their f_a, f_b in
+ * lb_init order) and of three 8-byte step counters in device memory. */
+typedef struct lb_peers {
+  double* left_buf[2];         /* left neighbour's f_a, f_b                    */
+  double* right_buf[2];        /* right neighbour's f_a, f_b                   */
+  const uint64_t* left_done;   /* left neighbour's step counter                */
+  const uint64_t* right_done;  /* right neighbour's step counter               */
+  uint64_t* my_done;           /* this rank's counter (read by both neighbours) */
+} lb_peers;
 
 typedef struct lb_ctx lb_ctx;
 
@@ -219,11 +233,26 @@ int lb_collide(lb_ctx* ctx);    /* in place on B (§8a4), THEN swaps A <-> B, so
 int lb_step(lb_ctx* ctx, int nsteps); /* nsteps full steps in p->mode, with the
                                    overlapped schedule when p->overlap         */
 
+/* Switch lb_step to the peer-store exchange: each step is ONE fused kernel
+ * whose 3+3 border-column blocks (i) wait until both neighbours' counters
+ * reach this rank's step index (their previous step is complete, so this
+ * rank's halo is current and theirs may be overwritten), (ii) compute, and
+ * (iii) also store their results into the neighbours' next buffers (left
+ * border -> left neighbour's right halo, right border -> right neighbour's
+ * left halo); bulk blocks never wait.  A one-thread kernel then publishes this
+ * rank's counter (st.release.sys).  Fused mode and walls only; per-rank
+ * lx >= 6.  Zeroes *my_done and synchronises.  Collective in effect: every
+ * rank calls it, then all ranks barrier before the next lb_step; the first
+ * step after it (or after lb_set_state / lb_init_macro, which must likewise be
+ * followed by a barrier) fills the halos by reading the neighbours' A. */
+int lb_set_peers(lb_ctx* ctx, const lb_peers* peers);
+
 /* ---- results ------------------------------------------------------------ */
 
 /* Collective over the ring.  Physical state A in canonical GLOBAL layout
  * [37][lx_total][Ly] written to host_out on rank `root` (other ranks may pass
- * NULL).  Uses B as device staging; only at a step boundary.  Synchronising. */
+ * NULL).  Uses B as device staging; only at a step boundary.  Synchronising.
+ * N > 1 needs the NCCL communicator (LB_ESTATE otherwise; use lb_peek). */
 int lb_gather(lb_ctx* ctx, double* host_out, int root);
 
 /* Debug view: this rank's physical sites of buffer which (0 = A, 1 = B) in
@@ -231,7 +260,8 @@ int lb_gather(lb_ctx* ctx, double* host_out, int root);
  * (e.g. between lb_propagate and lb_bc).  Synchronising. */
 int lb_peek(lb_ctx* ctx, int which, double* host_out);
 
-/* Collective.  out[0..3] = global sum over physical sites of rho, j_x, j_y
+/* Collective (local sums if the context has no NCCL communicator).
+ * out[0..3] = global sum over physical sites of rho, j_x, j_y
  * and E = 1/2 sum_l |c_l|^2 f_l, out[4] = global minimum site density.
  * Deterministic for a fixed N (fixed-order block partials).  Returns
  * LB_ENONPHYS if any value is NaN or min rho <= 0.  Synchronising. */

@@ -127,7 +127,11 @@ struct lb_ctx {
   double* d_part = nullptr;   // invariants partials (+5 result doubles)
   double* h_pin = nullptr;    // pinned 8 doubles for results
   int phase = 0;              // 0 = step boundary, 1 = after propagate, 2 = after bc
-  bool halo_fresh = false;    // A's x-halo columns already hold the wrap of A (N = 1)
+  bool halo_fresh = false;    // A's x-halo columns are current (wrap or peer stores)
+  int par = 0;                // A == caller's f_a if 0, f_b if 1 (toggles on swap)
+  bool peers_on = false;      // peer-store exchange (lb_set_peers)
+  lb_peers peers{};
+  uint64_t peer_step = 0;     // steps completed since lb_set_peers
   double omega = 1.0;
   int64_t launches = 0;
   // instrumentation
@@ -268,6 +272,7 @@ Cols border_cols(const lb_ctx* c) {
 int exchange_on(lb_ctx* c, cudaStream_t s) {
   const Geo& g = c->g;
   if (!c->comm) {
+    if (c->nranks > 1) return fail(LB_ESTATE, "N > 1 without an NCCL communicator: use lb_set_peers");
     return launch(c, "k_pbc_wrap", s, 6LL * g.ly, [&] {
       return lbk::launch_pbc_wrap(g, c->A, c->p.bc_y, s);
     });
@@ -285,10 +290,41 @@ int exchange_on(lb_ctx* c, cudaStream_t s) {
   return LB_OK;
 }
 
-int fused(lb_ctx* c, Cols cols, int wrap = 0) {
+int fused(lb_ctx* c, Cols cols, const lbk::Halo& h = lbk::Halo()) {
   return launch(c, c->p.collision ? "k_step_fused_reg" : "k_step_fused", c->s, (int64_t)cols.count() * c->g.ly, [&] {
-    return lbk::launch_step_fused(c->g, c->A, c->B, c->p.bc_y, c->p.collision, c->omega, cols, wrap, c->s);
+    return lbk::launch_step_fused(c->g, c->A, c->B, c->p.bc_y, c->p.collision, c->omega, cols, h, c->s);
   });
+}
+
+void swap_ab(lb_ctx* c) {
+  std::swap(c->A, c->B);
+  c->par ^= 1;
+}
+
+// Peer mode (lb_set_peers): one fused kernel per step whose border blocks
+// wait for both neighbours' previous step, pull their halo from this rank's A
+// and store their results into the neighbours' next buffers; then a one-thread
+// kernel publishes this rank's step counter.
+int step_peer(lb_ctx* c) {
+  const lb_peers& P = c->peers;
+  if (!c->halo_fresh)
+    TRY(launch(c, "k_peer_pull", c->s, 6LL * c->g.ly, [&] {
+      return lbk::launch_peer_pull(c->g, c->A, P.left_buf[c->par], P.right_buf[c->par], c->s);
+    }));
+  lbk::Halo h;
+  h.dstL = P.left_buf[c->par ^ 1];
+  h.dstR = P.right_buf[c->par ^ 1];
+  h.waitL = reinterpret_cast<const unsigned long long*>(P.left_done);
+  h.waitR = reinterpret_cast<const unsigned long long*>(P.right_done);
+  h.wait_val = c->peer_step;
+  TRY(fused(c, all_cols(c), h));
+  c->peer_step += 1;
+  TRY(launch(c, "k_signal", c->s, 0, [&] {
+    return lbk::launch_signal(reinterpret_cast<unsigned long long*>(P.my_done), c->peer_step, c->s);
+  }));
+  swap_ab(c);
+  c->halo_fresh = true;
+  return LB_OK;
 }
 
 int step_once(lb_ctx* c) {
@@ -298,13 +334,16 @@ int step_once(lb_ctx* c) {
     TRY(lb_bc(c));
     return lb_collide(c);
   }
+  if (c->peers_on) return step_peer(c);
   // N = 1 without NCCL, walls: the fused kernel writes the next step's halo
   // columns itself (one launch per step); a separate wrap only when A's halo
   // is stale (after lb_set_state / lb_init_macro / a split step).
-  if (!c->comm && c->p.bc_y != LB_PERIODIC) {
+  if (c->nranks == 1 && !c->comm && c->p.bc_y != LB_PERIODIC) {
     if (!c->halo_fresh) TRY(exchange_on(c, c->s));
-    TRY(fused(c, all_cols(c), 1));
-    std::swap(c->A, c->B);
+    lbk::Halo h;
+    h.dstL = h.dstR = c->B;
+    TRY(fused(c, all_cols(c), h));
+    swap_ab(c);
     c->halo_fresh = true;
     return LB_OK;
   }
@@ -325,7 +364,7 @@ int step_once(lb_ctx* c) {
     CU(cudaStreamWaitEvent(c->s, c->ev_comm, 0));
     TRY(fused(c, border_cols(c)));
   }
-  std::swap(c->A, c->B);
+  swap_ab(c);
   return LB_OK;
 }
 
@@ -418,7 +457,6 @@ int lb_init(const lb_params* p, const lb_dist* d, double* f_a, double* f_b, void
   TRY(validate(p, rank, nranks));
   if (!f_a || !f_b || f_a == f_b) return fail(LB_EINVAL, "need two distinct device buffers");
   if (((uintptr_t)f_a | (uintptr_t)f_b) & 15) return fail(LB_EINVAL, "buffers must be 16-byte aligned");
-  if (nranks > 1 && (!d || !d->nccl_id)) return fail(LB_EINVAL, "nranks > 1 needs an nccl_id");
   lb_ctx* c = new (std::nothrow) lb_ctx();
   if (!c) return fail(LB_ENOMEM, "host allocation failed");
   c->p = *p;
@@ -460,7 +498,7 @@ int lb_init(const lb_params* p, const lb_dist* d, double* f_a, double* f_b, void
   if (!gram_inverse(ginv)) return bail(fail(LB_EINVAL, "singular Gram matrix"));
   if (lbk::upload_ginv(ginv, c->s) != cudaSuccess)
     return bail(fail(LB_ECUDA, "constant upload failed"));
-  if (nranks > 1 || (d && d->nccl_id)) {
+  if (d && d->nccl_id) {
     ncclUniqueId id;
     std::memcpy(&id, d->nccl_id, 128);
     ncclResult_t r = ncclCommInitRank(&c->comm, nranks, id, rank);
@@ -585,7 +623,7 @@ int lb_collide(lb_ctx* c) {
   TRY(launch(c, c->p.collision ? "k_collide_reg" : "k_collide", c->s, c->L.sites, [&] {
     return lbk::launch_collide(c->g, c->B, c->omega, c->p.collision, c->s);
   }));
-  std::swap(c->A, c->B);
+  swap_ab(c);
   c->phase = 0;
   c->halo_fresh = false;
   return LB_OK;
@@ -609,6 +647,7 @@ int lb_gather(lb_ctx* c, double* host_out, int root) {
   TRY(check_boundary(c, "lb_gather"));
   if (root < 0 || root >= c->nranks) return fail(LB_EINVAL, "bad root %d", root);
   if (c->rank == root && !host_out) return fail(LB_EINVAL, "host_out is NULL on root");
+  if (c->nranks > 1 && !c->comm) return fail(LB_ESTATE, "lb_gather at N > 1 needs an NCCL communicator");
   const Geo& g = c->g;
   const int64_t blk = (int64_t)g.lx * g.ly;  // one plane of one rank
   const size_t dpitch = (size_t)c->p.lx_total * g.ly * sizeof(double);
@@ -673,6 +712,24 @@ int lb_invariants(lb_ctx* c, double* out) {
   for (int k = 0; k < 5; ++k)
     if (std::isnan(out[k])) return fail(LB_ENONPHYS, "NaN in invariants");
   if (!(out[4] > 0.0)) return fail(LB_ENONPHYS, "site density <= 0 or NaN");
+  return LB_OK;
+}
+
+int lb_set_peers(lb_ctx* c, const lb_peers* p) {
+  if (!c || !p) return fail(LB_EINVAL, "NULL argument");
+  if (c->phase != 0) return fail(LB_ESTATE, "lb_set_peers only at a step boundary");
+  if (c->p.mode != LB_MODE_FUSED || c->p.bc_y == LB_PERIODIC)
+    return fail(LB_EINVAL, "peer exchange needs fused mode and walls in Y");
+  if (c->g.lx < 6 && c->nranks > 1) return fail(LB_EINVAL, "peer exchange needs lx >= 6");
+  for (int k = 0; k < 2; ++k)
+    if (!p->left_buf[k] || !p->right_buf[k]) return fail(LB_EINVAL, "NULL peer buffer");
+  if (!p->left_done || !p->right_done || !p->my_done) return fail(LB_EINVAL, "NULL step counter");
+  c->peers = *p;
+  c->peers_on = true;
+  c->peer_step = 0;
+  c->halo_fresh = false;
+  CU(cudaMemsetAsync(p->my_done, 0, sizeof(uint64_t), c->s));
+  CU(cudaStreamSynchronize(c->s));
   return LB_OK;
 }
 

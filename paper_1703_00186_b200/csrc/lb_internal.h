@@ -35,8 +35,20 @@ cudaError_t launch_ywrap(const Geo& g, double* A, cudaStream_t s);
 cudaError_t launch_propagate(const Geo& g, const double* A, double* B, cudaStream_t s);
 cudaError_t launch_bc(const Geo& g, const double* A, double* B, int bc, cudaStream_t s);
 cudaError_t launch_collide(const Geo& g, double* B, double omega, int coll, cudaStream_t s);
+// Where the border columns' results also go (the next step's halos) and, in
+// peer mode, which step counters the border blocks wait on (lb_kernels.cu).
+struct Halo {
+  double* dstL = nullptr;   // ix in [3,6)      -> column ix + lx of dstL
+  double* dstR = nullptr;   // ix in [lx, lx+3) -> column ix - lx of dstR
+  const unsigned long long* waitL = nullptr;
+  const unsigned long long* waitR = nullptr;
+  unsigned long long wait_val = 0;
+};
 cudaError_t launch_step_fused(const Geo& g, const double* A, double* B, int bc, int coll,
-                              double omega, Cols cols, int wrap, cudaStream_t s);
+                              double omega, Cols cols, const Halo& h, cudaStream_t s);
+cudaError_t launch_signal(unsigned long long* done, unsigned long long v, cudaStream_t s);
+cudaError_t launch_peer_pull(const Geo& g, double* A, const double* left_A, const double* right_A,
+                             cudaStream_t s);
 cudaError_t launch_init_macro(const Geo& g, double* A, const double* rho, const double* ux,
                               const double* uy, const double* T, cudaStream_t s);
 cudaError_t launch_canon_to_internal(const Geo& g, const double* canon, double* A, cudaStream_t s);

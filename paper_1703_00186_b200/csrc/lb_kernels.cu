@@ -384,17 +384,59 @@ cudaError_t launch_collide(const Geo& g, double* B, double omega, int coll, cuda
 // gather (+mirror) -> thermal wall -> collide -> store, A -> B in one pass:
 // 296 B read + 296 B written per site.  Warps whose 32 rows are all at least
 // 3 rows from both walls take the mirror-free gather (warp-uniform branch).
-// wrap != 0 (N = 1 without NCCL): the blocks of the 3+3 border columns also
-// store their result into B's halo columns (pbc of the NEXT step done in the
-// producing kernel: left halo [0,3) <- [lx, lx+3), right halo [lx+3, lx+6) <-
-// [3, 6)), so the step needs no separate wrap launch.
+//
+// Halo h — the exchange of the NEXT step done by the producing kernel: the
+// blocks of the 3+3 border columns also store their result into the halo
+// columns of a destination buffer: ix in [3,6) -> column ix + lx of h.dstL
+// (the LEFT neighbour's next buffer: its right halo), ix in [lx, lx+3) ->
+// column ix - lx of h.dstR (the RIGHT neighbour's left halo).  N = 1 wrap:
+// dstL = dstR = own B.  Peer mode (N > 1, include/lb.h lb_set_peers): dstL /
+// dstR are the neighbours' buffers mapped into this process (NVLink P2P
+// stores), and before touching any halo the border blocks wait until both
+// neighbours have completed the previous step (h.waitL/R >= h.wait_val): that
+// both makes this rank's halo current and the neighbour's halo free to
+// overwrite.  Bulk blocks never wait, so the exchange overlaps the bulk inside
+// one grid (P:585-613 without a communication stream).
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <bool MIRROR>
+__device__ __forceinline__ void gather_cg(const double* A, const Geo& g, int ix, int y, double (&f)[Q]) {
+  // like gather<MIRROR> but with L2-coherent loads (halo data written by a
+  // peer during this kernel's lifetime must not go through the .nc path)
+  const int64_t b = (int64_t)ix * g.cs + g.y0 + y;
+#pragma unroll
+  for (int l = 0; l < Q; ++l) {
+    int plane = l;
+    int dy = -CY(l);
+    if (MIRROR) {
+      const int sy = y - CY(l);
+      if (sy < 0) { plane = refl(l); dy = (-1 - sy) - y; }
+      else if (sy >= g.ly) { plane = refl(l); dy = (2 * g.ly - 1 - sy) - y; }
+    }
+    const int64_t off = (int64_t)plane * g.nyp - (int64_t)CX(l) * g.cs + dy;
+    f[l] = __ldcg(A + b + off);
+  }
+}
+
 template <int BC, int COLL>
 __global__ void __launch_bounds__(TPB) k_step_fused(const double* __restrict__ A,
                                                     double* __restrict__ B, Geo g, Cols cols,
-                                                    double omega, double one_m_omega, int wrap) {
+                                                    double omega, double one_m_omega, Halo h) {
   const int y = blockIdx.x * TPB + threadIdx.x;
   const int na = cols.xa1 - cols.xa0;
   const int ix = (int)blockIdx.y < na ? cols.xa0 + (int)blockIdx.y : cols.xb0 + ((int)blockIdx.y - na);
+  const bool border = ix < 2 * H || ix >= g.lx;
+  const bool peer_wait = h.waitL != nullptr && border;
+  if (peer_wait) {  // block-uniform
+    if (threadIdx.x == 0) {
+      while (ld_acquire_sys(h.waitL) < h.wait_val || ld_acquire_sys(h.waitR) < h.wait_val) __nanosleep(128);
+    }
+    __syncthreads();
+  }
   if (y >= g.ly) return;
   double f[Q];
   if (BC == BC_PERIODIC) {
@@ -402,41 +444,79 @@ __global__ void __launch_bounds__(TPB) k_step_fused(const double* __restrict__ A
   } else {
     const int wy0 = blockIdx.x * TPB + (threadIdx.x & ~31);
     const bool interior = (wy0 >= 3) && (wy0 + 32 <= g.ly - 3);
-    if (interior) {
+    if (peer_wait) {
+      if (interior) gather_cg<false>(A, g, ix, y, f);
+      else gather_cg<true>(A, g, ix, y, f);
+    } else if (interior) {
       gather<false>(A, g, ix, y, f);
     } else {
       gather<true>(A, g, ix, y, f);
-      if (BC == BC_THERMAL && (y < 3 || y >= g.ly - 3)) thermal_wall(f, y < 3 ? 0 : 1);
     }
+    if (!interior && BC == BC_THERMAL && (y < 3 || y >= g.ly - 3)) thermal_wall(f, y < 3 ? 0 : 1);
   }
   collide_any<COLL>(f, omega, one_m_omega);
   store_site(B, g, ix, y, f);
-  if (wrap) {
-    if (ix < 2 * H) store_site(B, g, ix + g.lx, y, f);
-    if (ix >= g.lx) store_site(B, g, ix - g.lx, y, f);
-  }
+  if (h.dstL != nullptr && ix < 2 * H) store_site(h.dstL, g, ix + g.lx, y, f);
+  if (h.dstR != nullptr && ix >= g.lx) store_site(h.dstR, g, ix - g.lx, y, f);
+  if (peer_wait) __threadfence_system();  // remote halo stores performed before the step signal
 }
 
 template <int COLL>
 void launch_fused_bc(const Geo& g, const double* A, double* B, int bc, double omega, Cols cols,
-                     int wrap, dim3 grid, cudaStream_t s) {
+                     const Halo& h, dim3 grid, cudaStream_t s) {
   const double om1 = 1.0 - omega;
   switch (bc) {
-    case BC_THERMAL: k_step_fused<BC_THERMAL, COLL><<<grid, TPB, 0, s>>>(A, B, g, cols, omega, om1, wrap); break;
-    case BC_ADIABATIC: k_step_fused<BC_ADIABATIC, COLL><<<grid, TPB, 0, s>>>(A, B, g, cols, omega, om1, wrap); break;
-    default: k_step_fused<BC_PERIODIC, COLL><<<grid, TPB, 0, s>>>(A, B, g, cols, omega, om1, wrap); break;
+    case BC_THERMAL: k_step_fused<BC_THERMAL, COLL><<<grid, TPB, 0, s>>>(A, B, g, cols, omega, om1, h); break;
+    case BC_ADIABATIC: k_step_fused<BC_ADIABATIC, COLL><<<grid, TPB, 0, s>>>(A, B, g, cols, omega, om1, h); break;
+    default: k_step_fused<BC_PERIODIC, COLL><<<grid, TPB, 0, s>>>(A, B, g, cols, omega, om1, h); break;
   }
 }
 
 cudaError_t launch_step_fused(const Geo& g, const double* A, double* B, int bc, int coll,
-                              double omega, Cols cols, int wrap, cudaStream_t s) {
+                              double omega, Cols cols, const Halo& h, cudaStream_t s) {
   const int n = cols.count();
   if (n <= 0) return cudaSuccess;
   dim3 grid((g.ly + TPB - 1) / TPB, n);
   if (coll == COLL_REGULARIZED)
-    launch_fused_bc<COLL_REGULARIZED>(g, A, B, bc, omega, cols, wrap, grid, s);
+    launch_fused_bc<COLL_REGULARIZED>(g, A, B, bc, omega, cols, h, grid, s);
   else
-    launch_fused_bc<COLL_BGK>(g, A, B, bc, omega, cols, wrap, grid, s);
+    launch_fused_bc<COLL_BGK>(g, A, B, bc, omega, cols, h, grid, s);
+  return cudaGetLastError();
+}
+
+// Step signal of peer mode: this rank's counter := v (system-scope release),
+// after the fused kernel (stream order) and its border blocks' system fences.
+__global__ void k_signal(unsigned long long* done, unsigned long long v) {
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(done), "l"(v) : "memory");
+}
+
+cudaError_t launch_signal(unsigned long long* done, unsigned long long v, cudaStream_t s) {
+  k_signal<<<1, 1, 0, s>>>(done, v);
+  return cudaGetLastError();
+}
+
+// Initial halo fill of peer mode: A[0,3) <- left's A[lx, lx+3), A[lx+3, lx+6)
+// <- right's A[3, 6) (full columns; the caller guarantees the neighbours'
+// states are set and that no step is in flight).
+__global__ void k_peer_pull(double2* __restrict__ A, const double2* L, const double2* R, int64_t lx,
+                            int64_t cs2) {
+  const int64_t n = 3 * cs2;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 2 * n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < n)
+      A[i] = __ldcg(L + lx * cs2 + i);
+    else
+      A[(lx + 3) * cs2 + (i - n)] = __ldcg(R + 3 * cs2 + (i - n));
+  }
+}
+
+cudaError_t launch_peer_pull(const Geo& g, double* A, const double* left_A, const double* right_A,
+                             cudaStream_t s) {
+  const int64_t cs2 = g.cs / 2;
+  int blocks = (int)std::min<int64_t>((6 * cs2 + 255) / 256, 148 * 8);
+  k_peer_pull<<<blocks, 256, 0, s>>>(reinterpret_cast<double2*>(A), reinterpret_cast<const double2*>(left_A),
+                                     reinterpret_cast<const double2*>(right_A), g.lx, cs2);
   return cudaGetLastError();
 }
 

@@ -29,7 +29,7 @@ EXPORTS = ["lb_query_layout", "lb_exchange_plan", "lb_constants", "lb_kwall", "l
            "lb_strerror", "lb_init", "lb_destroy", "lb_get_layout", "lb_set_stream", "lb_init_macro",
            "lb_set_state", "lb_exchange", "lb_propagate", "lb_bc", "lb_collide", "lb_step",
            "lb_gather", "lb_peek", "lb_invariants", "lb_sync", "lb_profile_enable",
-           "lb_profile_reset", "lb_profile_read", "lb_launch_count"]
+           "lb_profile_reset", "lb_profile_read", "lb_launch_count", "lb_set_peers"]
 
 
 class LBError(RuntimeError):
@@ -62,6 +62,12 @@ class lb_xplan(ctypes.Structure):
                 ("bulk_x0", ctypes.c_int), ("bulk_x1", ctypes.c_int),
                 ("border_x0", ctypes.c_int), ("border_x1", ctypes.c_int),
                 ("border_x2", ctypes.c_int), ("border_x3", ctypes.c_int)]
+
+
+class lb_peers(ctypes.Structure):
+    _fields_ = [("left_buf", ctypes.c_void_p * 2), ("right_buf", ctypes.c_void_p * 2),
+                ("left_done", ctypes.c_void_p), ("right_done", ctypes.c_void_p),
+                ("my_done", ctypes.c_void_p)]
 
 
 class lb_kprof(ctypes.Structure):
@@ -106,6 +112,7 @@ def lib():
         "lb_profile_enable": (i, [vp, i]), "lb_profile_reset": (i, [vp]),
         "lb_profile_read": (i, [vp, p(lb_kprof), i, p(i)]),
         "lb_launch_count": (ctypes.c_int64, [vp]),
+        "lb_set_peers": (i, [vp, p(lb_peers)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -317,6 +324,32 @@ class Lattice:
         _check(lib().lb_profile_read(self._ctx, recs, 64, ctypes.byref(n)))
         return {recs[i].name.decode(): {"launches": recs[i].launches, "total_ms": recs[i].total_ms,
                                         "units": recs[i].units} for i in range(min(n.value, 64))}
+
+    def set_peers(self, left, right):
+        """Peer-store exchange with neighbour lattices of THIS process (same
+        device): left/right are Lattice objects (may be self).  Every rank must
+        call it before any of them steps."""
+        import torch
+        if not hasattr(self, "done"):
+            self.done = torch.zeros(1, dtype=torch.int64, device=self.device)
+        for nb in (left, right):
+            if not hasattr(nb, "done"):
+                nb.done = torch.zeros(1, dtype=torch.int64, device=nb.device)
+        P = lb_peers()
+        P.left_buf[0], P.left_buf[1] = left.bufs[0].data_ptr(), left.bufs[1].data_ptr()
+        P.right_buf[0], P.right_buf[1] = right.bufs[0].data_ptr(), right.bufs[1].data_ptr()
+        P.left_done, P.right_done = left.done.data_ptr(), right.done.data_ptr()
+        P.my_done = self.done.data_ptr()
+        self._peers = (left, right)
+        _check(lib().lb_set_peers(self._ctx, ctypes.byref(P)))
+
+    def set_peers_raw(self, left_bufs, right_bufs, left_done, right_done, my_done):
+        """Peer-store exchange from raw device pointers (e.g. CUDA IPC mappings)."""
+        P = lb_peers()
+        P.left_buf[0], P.left_buf[1] = left_bufs
+        P.right_buf[0], P.right_buf[1] = right_bufs
+        P.left_done, P.right_done, P.my_done = left_done, right_done, my_done
+        _check(lib().lb_set_peers(self._ctx, ctypes.byref(P)))
 
     def launch_count(self) -> int:
         return int(lib().lb_launch_count(self._ctx))

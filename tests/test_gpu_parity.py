@@ -314,3 +314,42 @@ def test_regularized_split_fused_bit_identical_and_256(lb):
     o.init_macro(*fields)
     o.step(3)
     assert max_rel(outs[1], o.get_state(0)) < TOL
+
+
+# ------------------------------------------------------------------ peer-store exchange (NEXT 3)
+
+@pytest.mark.parametrize("nranks,streams,coll", [(2, "separate", "bgk"), (3, "separate", "regularized"),
+                                                 (4, "shared", "bgk"), (1, "separate", "bgk")])
+def test_peer_exchange_ring_equals_single_lattice(lb, nranks, streams, coll):
+    """N X-slabs in one process on one GPU, exchanging halos only through the
+    fused kernel's peer stores + step counters (lb_set_peers): after several
+    steps the slabs equal the 1-slab run bit for bit, and the oracle."""
+    lx, ly, nsteps = 24, 70, 9
+    lx_total = lx * nranks
+    T0 = oracle.t0()
+    ref = lb.Lattice(lx_total, ly, collision=coll)
+    ref.init_macro(*lbgen.rt_macro(lx_total, ly, T0))
+    ref.step(nsteps)
+    want = ref.gather()
+    ranks = []
+    for r in range(nranks):
+        st = torch.cuda.Stream() if streams == "separate" else None
+        g = lb.Lattice(lx_total, ly, rank=r, nranks=nranks, stream=st, collision=coll)
+        g.init_macro(*lbgen.rt_macro(lx_total, ly, T0, x0=r * lx, lx=lx))
+        ranks.append(g)
+    for r, g in enumerate(ranks):
+        g.set_peers(ranks[(r - 1) % nranks], ranks[(r + 1) % nranks])
+    torch.cuda.synchronize()
+    for _ in range(nsteps):
+        for g in ranks:
+            g.step(1)
+    for g in ranks:
+        g.sync()
+    got = np.concatenate([g.peek(0) for g in ranks], axis=1)
+    assert np.array_equal(got, want)
+    o = oracle.Lattice(lx_total, ly, collision=oracle.REGULARIZED if coll == "regularized" else oracle.BGK)
+    o.init_macro(*lbgen.rt_macro(lx_total, ly, T0))
+    o.step(nsteps)
+    assert max_rel(got, o.get_state(0)) < TOL
+    for g in ranks:
+        g.close()
