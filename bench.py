@@ -226,6 +226,9 @@ def main():
     ap.add_argument("--config", default="weak1920", choices=sorted(CONFIGS))
     ap.add_argument("--mode", default="fused", choices=["fused", "split"])
     ap.add_argument("--overlap", type=int, default=-1, help="-1: auto (on for N>1)")
+    ap.add_argument("--transport", default="auto", choices=["auto", "peer", "nccl"],
+                    help="N>1 halo exchange: peer stores fused into the step kernel (CUDA IPC over "
+                         "NVLink, default) or NCCL send/recv on a comm stream overlapped with the bulk")
     ap.add_argument("--no-extras", action="store_true", help="skip e2e / split pass / cpu baseline")
     args = ap.parse_args()
     if args.warmup < 3:
@@ -271,9 +274,17 @@ def main():
 
     T0 = lb.t0()
     g = lb.Lattice(lx_total, ly, mode=args.mode, overlap=overlap, rank=rank, nranks=world, nccl_id=nccl_id)
+    transport = "local" if world == 1 else ("nccl" if args.transport == "nccl" or args.mode != "fused" else "peer")
     lx = g.lx
     fields = lbgen.rt_macro(lx_total, ly, T0, x0=rank * lx, lx=lx)
     g.init_macro(*fields)
+    if transport == "peer":
+        try:
+            g.set_peers_ipc()
+        except Exception as exc:  # fall back to the NCCL ring (communicator exists)
+            print(f"peer exchange unavailable ({exc}); using NCCL", file=sys.stderr)
+            transport = "nccl"
+    barrier()
     stream = torch.cuda.current_stream()
 
     # ---- warm-up, then exactly K timed steps (device time, max over ranks)
@@ -336,6 +347,7 @@ def main():
                             for k, v in prof.items()},
     }
     line["config"]["overlap"] = overlap
+    line["config"]["transport"] = transport
 
     if not args.no_extras:
         # ---- e2e through the C ABI with pinned host buffers (same fused path)
@@ -351,6 +363,7 @@ def main():
         torch.cuda.synchronize()
         t = time.perf_counter()
         g.set_state(host_in.numpy())
+        barrier()  # peer mode: neighbours' states set before the first halo pull
         for _ in range(k_e2e):
             g.step(1)
             g.invariants()

@@ -343,6 +343,34 @@ class Lattice:
         self._peers = (left, right)
         _check(lib().lb_set_peers(self._ctx, ctypes.byref(P)))
 
+    def set_peers_ipc(self, group=None):
+        """Peer-store exchange across processes (one rank per GPU, or several
+        ranks sharing a GPU): every rank's buffers and step counter are shared
+        with CUDA IPC (torch.multiprocessing's tensor reduction, which opens the
+        handles with lazy peer access, i.e. NVLink P2P mappings), exchanged with
+        torch.distributed.all_gather_object; then lb_set_peers and a barrier.
+        Collective over the ring's process group."""
+        import torch
+        import torch.distributed as dist
+        from torch.multiprocessing.reductions import reduce_tensor
+        if not hasattr(self, "done"):
+            self.done = torch.zeros(1, dtype=torch.int64, device=self.device)
+        mine = [reduce_tensor(t) for t in (self.bufs[0], self.bufs[1], self.done)]
+        allr = [None] * self.nranks
+        dist.all_gather_object(allr, mine, group=group)
+        left, right = (self.rank - 1) % self.nranks, (self.rank + 1) % self.nranks
+
+        def open_rank(r):
+            if r == self.rank:
+                return [self.bufs[0], self.bufs[1], self.done]
+            return [fn(*args) for fn, args in allr[r]]
+
+        L, R = open_rank(left), open_rank(right)
+        self._peer_tensors = (L, R)  # keep the IPC mappings alive
+        self.set_peers_raw((L[0].data_ptr(), L[1].data_ptr()), (R[0].data_ptr(), R[1].data_ptr()),
+                           L[2].data_ptr(), R[2].data_ptr(), self.done.data_ptr())
+        dist.barrier(group=group)
+
     def set_peers_raw(self, left_bufs, right_bufs, left_done, right_done, my_done):
         """Peer-store exchange from raw device pointers (e.g. CUDA IPC mappings)."""
         P = lb_peers()
