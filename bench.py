@@ -251,8 +251,16 @@ def main():
     import lbgen
     import paper_1703_00186_b200 as lb
 
-    torch.cuda.set_device(local_rank)
-    if world > 1:
+    # LB_BENCH_SAME_GPU=1 (test only): all ranks on cuda:0, gloo process group,
+    # no NCCL communicator, peer transport -- exercises the N > 1 code path of
+    # this script on a one-GPU box (numbers meaningless: ranks time-slice).
+    same_gpu = os.environ.get("LB_BENCH_SAME_GPU") == "1" and world > 1
+    dev_index = 0 if same_gpu else local_rank
+    torch.cuda.set_device(dev_index)
+    if world > 1 and same_gpu:
+        dist.init_process_group("gloo")
+        nccl_id = None
+    elif world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         obj = [lb.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
@@ -268,7 +276,7 @@ def main():
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if same_gpu else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -282,6 +290,8 @@ def main():
         try:
             g.set_peers_ipc()
         except Exception as exc:  # fall back to the NCCL ring (communicator exists)
+            if same_gpu:
+                raise
             print(f"peer exchange unavailable ({exc}); using NCCL", file=sys.stderr)
             transport = "nccl"
     barrier()
@@ -296,7 +306,7 @@ def main():
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local_rank) as clk:
+    with ClockSampler(dev_index) as clk:
         e0.record(stream)
         g.step(args.steps)
         e1.record(stream)
@@ -348,6 +358,8 @@ def main():
     }
     line["config"]["overlap"] = overlap
     line["config"]["transport"] = transport
+    if same_gpu:
+        line["config"]["same_gpu_test"] = "all ranks on cuda:0 (test of the N>1 code path, not a measurement)"
 
     if not args.no_extras:
         # ---- e2e through the C ABI with pinned host buffers (same fused path)
@@ -367,7 +379,10 @@ def main():
         for _ in range(k_e2e):
             g.step(1)
             g.invariants()
-        g.gather(out=host_out.numpy() if host_out is not None else None)
+        if same_gpu:
+            g.peek(0)   # no communicator: each rank reads its own slab back
+        else:
+            g.gather(out=host_out.numpy() if host_out is not None else None)
         e2e_s = max_over_ranks(time.perf_counter() - t)
         line["e2e"] = {"value": round(sites_all * k_e2e / e2e_s / 1e6, 2), "unit": "MLUPS",
                        "h2d_bytes_per_step": state_bytes / k_e2e,

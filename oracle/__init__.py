@@ -56,6 +56,7 @@ def lib():
             "lbref_macro": (v, [p, p]), "lbref_feq": (v, [d, d, d, d, p]),
             "lbref_kwall": (v, [d, p]), "lbref_collide_site": (v, [p, d]),
             "lbref_project": (v, [p, p]), "lbref_collide_site_reg": (v, [p, d]),
+            "lbref_collide_site_force": (v, [p, d, d, d, i]), "lbref_set_gravity": (v, [p, d, d]),
             "lbref_init": (p, [i, i, d, d, d, d, i, i]), "lbref_free": (v, [p]),
             "lbref_nx": (i, [p]), "lbref_ny": (i, [p]), "lbref_buffer": (dp, [p, i]),
             "lbref_set_state": (v, [p, p]), "lbref_get_state": (v, [p, i, p]),
@@ -143,6 +144,13 @@ def project(f) -> np.ndarray:
     return out
 
 
+def collide_site_force(f, omega, gx, gy, collision=BGK) -> np.ndarray:
+    """Collide with body force g: shifted equilibrium (reading G7b)."""
+    f = np.array(f, dtype=np.float64)
+    lib().lbref_collide_site_force(_ptr(f), float(omega), float(gx), float(gy), int(collision))
+    return f
+
+
 def collide_site_reg(f, omega) -> np.ndarray:
     """Regularised collide: f_eq + (1 - omega)(P f - f_eq)."""
     f = np.array(f, dtype=np.float64)
@@ -156,7 +164,7 @@ class Lattice:
     """One slab (N=1) of the canonical layout [37][Lx+6][Ly+6]."""
 
     def __init__(self, lx, ly, tau=0.8, dt=1.0, t_bottom=None, t_top=None, bc_y=WALL_THERMAL,
-                 collision=BGK):
+                 collision=BGK, gravity=(0.0, 0.0)):
         T0 = t0()
         t_bottom = 1.05 * T0 if t_bottom is None else t_bottom
         t_top = 0.95 * T0 if t_top is None else t_top
@@ -164,6 +172,7 @@ class Lattice:
         self._h = lib().lbref_init(lx, ly, tau, dt, t_bottom, t_top, bc_y, collision)
         if not self._h:
             raise ValueError("lbref_init rejected the parameters")
+        lib().lbref_set_gravity(self._h, float(gravity[0]), float(gravity[1]))
         self.nx = lib().lbref_nx(self._h)
         self.ny = lib().lbref_ny(self._h)
 

@@ -236,11 +236,33 @@ void lbref_collide_site_reg(double f[Q], double omega)
     for (int l = 0; l < Q; ++l) f[l] = feq[l] + (1.0 - omega) * (pf[l] - feq[l]);
 }
 
+/* Body force (reading G7b; NEXT 2): the shifted-equilibrium scheme of the
+ * D2Q37 thermal model of the paper's reference [JFM]: with
+ * tau = 1/omega, f_eq is evaluated at u + tau g and at
+ * T + tau (1 - tau) |g|^2 / D, so that one collision adds exactly rho g to the
+ * momentum and rho (u.g + |g|^2/2) to the energy of the site. */
+void lbref_collide_site_force(double f[Q], double omega, double gx, double gy, int collision)
+{
+    const double tau = 1.0 / omega;
+    double m[4], feq[Q];
+    lbref_macro(f, m);
+    const double ux = m[1] + tau * gx, uy = m[2] + tau * gy;
+    const double T = m[3] + tau * (1.0 - tau) * (gx * gx + gy * gy) / D;
+    lbref_feq(m[0], ux, uy, T, feq);
+    if (collision == LBREF_REGULARIZED) {
+        double pf[Q];
+        lbref_project(f, pf);
+        for (int l = 0; l < Q; ++l) f[l] = feq[l] + (1.0 - omega) * (pf[l] - feq[l]);
+    } else {
+        for (int l = 0; l < Q; ++l) f[l] = f[l] - omega * (f[l] - feq[l]);
+    }
+}
+
 /* ------------------------------------------------------------------------ */
 
 struct lbref {
     int lx, ly, nx, ny, bc_y, collision;
-    double omega, t_bottom, t_top;
+    double omega, t_bottom, t_top, gx, gy;
     double *a, *b;            /* canonical [Q][NX][NY] */
     int c[Q][2];
     int refl[Q];
@@ -291,6 +313,12 @@ void lbref_free(lbref* s)
     free(s->a);
     free(s->b);
     free(s);
+}
+
+void lbref_set_gravity(lbref* s, double gx, double gy)
+{
+    s->gx = gx;
+    s->gy = gy;
 }
 
 int lbref_nx(const lbref* s) { return s->nx; }
@@ -403,7 +431,9 @@ void lbref_collide(lbref* s)
         for (int iy = HY; iy < HY + s->ly; ++iy) {
             double f[Q];
             for (int l = 0; l < Q; ++l) f[l] = s->b[IDX(s, l, ix, iy)];
-            if (s->collision == LBREF_REGULARIZED)
+            if (s->gx != 0.0 || s->gy != 0.0)
+                lbref_collide_site_force(f, s->omega, s->gx, s->gy, s->collision);
+            else if (s->collision == LBREF_REGULARIZED)
                 lbref_collide_site_reg(f, s->omega);
             else
                 lbref_collide_site(f, s->omega);

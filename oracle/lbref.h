@@ -52,6 +52,11 @@ void   lbref_collide_site(double f[LBREF_Q], double omega);
 void   lbref_project(const double f[LBREF_Q], double out[LBREF_Q]);
 /* Regularised collide in place: f <- f_eq + (1 - omega)(P f - f_eq)          */
 void   lbref_collide_site_reg(double f[LBREF_Q], double omega);
+/* Collide with a body force g (reading G7b: shifted equilibrium,
+ * dt = 1, tau = 1/omega): f_eq is evaluated at u + tau g and
+ * T + tau (1 - tau) |g|^2 / D.  collision = LBREF_BGK or LBREF_REGULARIZED.  */
+void   lbref_collide_site_force(double f[LBREF_Q], double omega, double gx, double gy,
+                                int collision);
 
 /* ---- lattice stepper --------------------------------------------------- */
 enum { LBREF_BGK = 0, LBREF_REGULARIZED = 1 };
@@ -59,6 +64,8 @@ enum { LBREF_BGK = 0, LBREF_REGULARIZED = 1 };
 lbref* lbref_init(int lx, int ly, double tau, double dt,
                   double t_bottom, double t_top, int bc_y, int collision);
 void   lbref_free(lbref*);
+/* body force per unit mass (lattice units), default 0 (reading G7b)          */
+void   lbref_set_gravity(lbref*, double gx, double gy);
 int    lbref_nx(const lbref*);
 int    lbref_ny(const lbref*);
 double* lbref_buffer(lbref*, int which);       /* canonical [37][NX][NY]     */

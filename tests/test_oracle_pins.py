@@ -478,3 +478,47 @@ def test_regularized_periodic_step_conserves_invariants():
     L.step(50)
     inv = L.invariants(0)
     assert np.abs(inv - inv0).max() / inv0[0] < 1e-13
+
+
+# ---------------------------------------------------------------- body force (NEXT 2, G7b)
+
+@pytest.mark.parametrize("coll", [oracle.BGK, oracle.REGULARIZED])
+@pytest.mark.parametrize("omega", [1.25, 1.0, 0.7])
+def test_force_adds_exact_momentum_and_work(coll, omega):
+    """One forced collision adds rho g to the momentum and rho (u.g + |g|^2/2) to
+    E = 1/2 sum |c|^2 f, conserves mass — the balance laws of a body force."""
+    c = oracle.velocities().astype(float)
+    c2 = (c ** 2).sum(axis=1)
+    gx, gy = 3e-5, -2e-4
+    f = _near_eq_f(31)
+    rho = f.sum()
+    u = (c.T @ f) / rho
+    g = oracle.collide_site_force(f, omega, gx, gy, coll)
+    assert abs(g.sum() - rho) < 1e-14 * rho
+    assert np.allclose(c.T @ g - c.T @ f, [rho * gx, rho * gy], rtol=1e-9, atol=1e-17)
+    dE = 0.5 * c2 @ g - 0.5 * c2 @ f
+    assert abs(dE - rho * (u @ [gx, gy] + 0.5 * (gx * gx + gy * gy))) < 1e-14 * (0.5 * c2 @ f)
+
+
+def test_force_zero_reduces_to_unforced():
+    f = _near_eq_f(32)
+    assert np.array_equal(oracle.collide_site_force(f, 1.25, 0.0, 0.0, oracle.BGK), oracle.collide_site(f, 1.25))
+    assert np.array_equal(oracle.collide_site_force(f, 1.25, 0.0, 0.0, oracle.REGULARIZED),
+                          oracle.collide_site_reg(f, 1.25))
+
+
+def test_uniform_fluid_free_fall_closed_form():
+    """Periodic box, uniform fluid at rest, gravity g: every site stays identical
+    and the momentum grows linearly, j(n) = n rho g (closed form)."""
+    lx, ly, n = 6, 8, 40
+    gy = -1e-4
+    L = oracle.Lattice(lx, ly, bc_y=oracle.PERIODIC, gravity=(0.0, gy))
+    ones = np.ones((lx, ly))
+    L.init_macro(ones, 0 * ones, 0 * ones, oracle.t0() * ones)
+    L.step(n)
+    inv = L.invariants(0)
+    sites = lx * ly
+    assert abs(inv[0] - sites) < 1e-12 * sites
+    assert abs(inv[2] - n * sites * gy) < 1e-10 * abs(n * sites * gy)
+    st = L.get_state(0)
+    assert np.abs(st - st[:, :1, :1]).max() < 1e-15
