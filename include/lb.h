@@ -101,6 +101,9 @@ typedef struct lb_params {
   int mode;              /* enum lb_mode                                       */
   int overlap;           /* 1: exchange || bulk, then borders     */
   int collision;         /* enum lb_collision                                 */
+  double gx, gy;         /* body force: velocity increment per step (NEXT 2,
+                            shifted equilibrium u + tau g, T + tau(1-tau)|g|^2/D;
+                            DESIGN.md reading G7b); 0 = unforced Eq. 1         */
 } lb_params;
 
 typedef struct lb_dist {

@@ -133,6 +133,7 @@ struct lb_ctx {
   lb_peers peers{};
   uint64_t peer_step = 0;     // steps completed since lb_set_peers
   double omega = 1.0;
+  lbd::Relax relax{};
   int64_t launches = 0;
   // instrumentation
   bool prof = false;
@@ -218,6 +219,7 @@ int validate(const lb_params* p, int rank, int nranks) {
   if (p->ly < (p->bc_y == LB_PERIODIC ? 3 : 6)) return fail(LB_EINVAL, "ly = %d too small", p->ly);
   if (p->mode < 0 || p->mode > 1) return fail(LB_EINVAL, "bad mode");
   if (p->collision < 0 || p->collision > 1) return fail(LB_EINVAL, "bad collision");
+  if (!std::isfinite(p->gx) || !std::isfinite(p->gy)) return fail(LB_EINVAL, "gravity must be finite");
   if (!(p->tau > 0.0) || !(p->dt > 0.0)) return fail(LB_EINVAL, "tau and dt must be > 0");
   const double om = p->dt / p->tau;
   if (!(om > 0.0 && om <= 2.0)) return fail(LB_EINVAL, "dt/tau must be in (0, 2]");
@@ -292,7 +294,7 @@ int exchange_on(lb_ctx* c, cudaStream_t s) {
 
 int fused(lb_ctx* c, Cols cols, const lbk::Halo& h = lbk::Halo()) {
   return launch(c, c->p.collision ? "k_step_fused_reg" : "k_step_fused", c->s, (int64_t)cols.count() * c->g.ly, [&] {
-    return lbk::launch_step_fused(c->g, c->A, c->B, c->p.bc_y, c->p.collision, c->omega, cols, h, c->s);
+    return lbk::launch_step_fused(c->g, c->A, c->B, c->p.bc_y, c->p.collision, c->relax, cols, h, c->s);
   });
 }
 
@@ -471,6 +473,15 @@ int lb_init(const lb_params* p, const lb_dist* d, double* f_a, double* f_b, void
   c->B = f_b;
   c->s = (cudaStream_t)stream;
   c->omega = p->dt / p->tau;
+  {
+    // body force (reading G7b): u_eq = u + g/omega, T_eq = T + (1/omega)(1 - 1/omega)|g|^2/D
+    const double it = 1.0 / c->omega;
+    c->relax.omega = c->omega;
+    c->relax.one_m_omega = 1.0 - c->omega;
+    c->relax.tgx = it * p->gx;
+    c->relax.tgy = it * p->gy;
+    c->relax.dT = it * (1.0 - it) * (p->gx * p->gx + p->gy * p->gy) / 2.0;
+  }
   auto bail = [&](int code) {
     lb_destroy(c);
     return code;
@@ -621,7 +632,7 @@ int lb_collide(lb_ctx* c) {
   if (c->phase != 2 && !(c->phase == 1 && c->p.bc_y == LB_PERIODIC))
     return fail(LB_ESTATE, "lb_collide must follow lb_bc");
   TRY(launch(c, c->p.collision ? "k_collide_reg" : "k_collide", c->s, c->L.sites, [&] {
-    return lbk::launch_collide(c->g, c->B, c->omega, c->p.collision, c->s);
+    return lbk::launch_collide(c->g, c->B, c->relax, c->p.collision, c->s);
   }));
   swap_ab(c);
   c->phase = 0;

@@ -127,6 +127,14 @@ struct Macro {
   double rho, ux, uy, T;
 };
 
+// Relaxation parameters of one launch: omega = dt/tau, 1 - omega, and the
+// body-force shift of the equilibrium (reading G7b): u_eq = u + (tgx, tgy)
+// with (tgx, tgy) = g/omega, T_eq = T + dT with dT = (1/omega)(1 - 1/omega)|g|^2/D.
+// With g = 0 the shifts are exact zeros and the arithmetic is unchanged.
+struct Relax {
+  double omega, one_m_omega, tgx, tgy, dT;
+};
+
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
@@ -203,11 +211,13 @@ __device__ __forceinline__ double cu_of(int l, double Ux, double Uy) {
 }
 
 // f <- f - omega (f - f_eq(moments of f)), in registers.
-__device__ __forceinline__ void collide_site(double (&f)[Q], double omega, double one_m_omega) {
+__device__ __forceinline__ void collide_site(double (&f)[Q], const Relax& r) {
+  const double omega = r.omega, one_m_omega = r.one_m_omega;
   const Macro m = moments(f);
-  const double Ux = dmul(A2, m.ux), Uy = dmul(A2, m.uy);
-  const double u2 = dmul(A2, dfma(m.ux, m.ux, dmul(m.uy, m.uy)));
-  const double t = dfma(A2, m.T, -1.0);
+  const double ux = dadd(m.ux, r.tgx), uy = dadd(m.uy, r.tgy), Te = dadd(m.T, r.dT);
+  const double Ux = dmul(A2, ux), Uy = dmul(A2, uy);
+  const double u2 = dmul(A2, dfma(ux, ux, dmul(uy, uy)));
+  const double t = dfma(A2, Te, -1.0);
   Shell sh[NSHELL];
   shell_coeffs(u2, t, sh);
   const double orho = dmul(omega, m.rho);

@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 
+#include "lb_device.cuh"
+
 namespace lbk {
 
 // Geometry of one rank's internal buffers (see include/lb.h "internal").
@@ -34,7 +36,7 @@ cudaError_t launch_pbc_wrap(const Geo& g, double* A, int bc, cudaStream_t s);
 cudaError_t launch_ywrap(const Geo& g, double* A, cudaStream_t s);
 cudaError_t launch_propagate(const Geo& g, const double* A, double* B, cudaStream_t s);
 cudaError_t launch_bc(const Geo& g, const double* A, double* B, int bc, cudaStream_t s);
-cudaError_t launch_collide(const Geo& g, double* B, double omega, int coll, cudaStream_t s);
+cudaError_t launch_collide(const Geo& g, double* B, const lbd::Relax& r, int coll, cudaStream_t s);
 // Where the border columns' results also go (the next step's halos) and, in
 // peer mode, which step counters the border blocks wait on (lb_kernels.cu).
 struct Halo {
@@ -45,7 +47,7 @@ struct Halo {
   unsigned long long wait_val = 0;
 };
 cudaError_t launch_step_fused(const Geo& g, const double* A, double* B, int bc, int coll,
-                              double omega, Cols cols, const Halo& h, cudaStream_t s);
+                              const lbd::Relax& r, Cols cols, const Halo& h, cudaStream_t s);
 cudaError_t launch_signal(unsigned long long* done, unsigned long long v, cudaStream_t s);
 cudaError_t launch_peer_pull(const Geo& g, double* A, const double* left_A, const double* right_A,
                              cudaStream_t s);

@@ -47,7 +47,8 @@ LB_HD constexpr double ipow(int c, int p) {
 // M'_a = (1 - omega) M_a(f) + omega rho m_p(ux, T) m_q(uy, T): the raw moments
 // of f blended with the Maxwellian moments that f_eq reproduces exactly
 // (m_k(u, T) = E[(u + sqrt(T) Z)^k], lattice units).
-__device__ __forceinline__ void collide_site_reg(double (&f)[Q], double omega, double one_m_omega) {
+__device__ __forceinline__ void collide_site_reg(double (&f)[Q], const Relax& r) {
+  const double omega = r.omega, one_m_omega = r.one_m_omega;
   // 1. column sums T[cx+3][q] = sum_{l: cx_l = cx} cy_l^q f_l
   double T[7][5];
   {
@@ -96,8 +97,10 @@ __device__ __forceinline__ void collide_site_reg(double (&f)[Q], double omega, d
   // 3. macroscopic fields (Eq. 2): rho, u, T = (e/rho - |u|^2)/2
   const double rho = M[0];
   const double inv = __drcp_rn(rho);
-  const double ux = dmul(M[6], inv), uy = dmul(M[9], inv);
-  const double Tm = dmul(0.5, dsub(dmul(dadd(M[1], M[2]), inv), dfma(ux, ux, dmul(uy, uy))));
+  const double ux0 = dmul(M[6], inv), uy0 = dmul(M[9], inv);
+  const double Tm0 = dmul(0.5, dsub(dmul(dadd(M[1], M[2]), inv), dfma(ux0, ux0, dmul(uy0, uy0))));
+  // equilibrium arguments with the body-force shift (G7b)
+  const double ux = dadd(ux0, r.tgx), uy = dadd(uy0, r.tgy), Tm = dadd(Tm0, r.dT);
   // 4. Maxwellian moments per axis
   double mx[5], my[5];
   {
@@ -349,16 +352,15 @@ cudaError_t launch_bc(const Geo& g, const double* A, double* B, int bc, cudaStre
 
 // ---------------------------------------------------------------- collide (§8a4)
 template <int COLL>
-__device__ __forceinline__ void collide_any(double (&f)[Q], double omega, double one_m_omega) {
+__device__ __forceinline__ void collide_any(double (&f)[Q], const Relax& r) {
   if (COLL == COLL_REGULARIZED)
-    collide_site_reg(f, omega, one_m_omega);
+    collide_site_reg(f, r);
   else
-    collide_site(f, omega, one_m_omega);
+    collide_site(f, r);
 }
 
 template <int COLL>
-__global__ void __launch_bounds__(TPB) k_collide(double* __restrict__ B, Geo g, double omega,
-                                                 double one_m_omega) {
+__global__ void __launch_bounds__(TPB) k_collide(double* __restrict__ B, Geo g, Relax r) {
   const int y = blockIdx.x * TPB + threadIdx.x;
   const int ix = H + blockIdx.y;
   if (y >= g.ly) return;
@@ -366,17 +368,17 @@ __global__ void __launch_bounds__(TPB) k_collide(double* __restrict__ B, Geo g, 
   double f[Q];
 #pragma unroll
   for (int l = 0; l < Q; ++l) f[l] = p[(int64_t)l * g.nyp];
-  collide_any<COLL>(f, omega, one_m_omega);
+  collide_any<COLL>(f, r);
 #pragma unroll
   for (int l = 0; l < Q; ++l) p[(int64_t)l * g.nyp] = f[l];
 }
 
-cudaError_t launch_collide(const Geo& g, double* B, double omega, int coll, cudaStream_t s) {
+cudaError_t launch_collide(const Geo& g, double* B, const Relax& r, int coll, cudaStream_t s) {
   dim3 grid((g.ly + TPB - 1) / TPB, g.lx);
   if (coll == COLL_REGULARIZED)
-    k_collide<COLL_REGULARIZED><<<grid, TPB, 0, s>>>(B, g, omega, 1.0 - omega);
+    k_collide<COLL_REGULARIZED><<<grid, TPB, 0, s>>>(B, g, r);
   else
-    k_collide<COLL_BGK><<<grid, TPB, 0, s>>>(B, g, omega, 1.0 - omega);
+    k_collide<COLL_BGK><<<grid, TPB, 0, s>>>(B, g, r);
   return cudaGetLastError();
 }
 
@@ -423,9 +425,9 @@ __device__ __forceinline__ void gather_cg(const double* A, const Geo& g, int ix,
 }
 
 template <int BC, int COLL>
-__global__ void __launch_bounds__(TPB) k_step_fused(const double* __restrict__ A,
+__global__ void __launch_bounds__(TPB, BC == BC_PERIODIC ? 3 : 4) k_step_fused(const double* __restrict__ A,
                                                     double* __restrict__ B, Geo g, Cols cols,
-                                                    double omega, double one_m_omega, Halo h) {
+                                                    Relax r, Halo h) {
   const int y = blockIdx.x * TPB + threadIdx.x;
   const int na = cols.xa1 - cols.xa0;
   const int ix = (int)blockIdx.y < na ? cols.xa0 + (int)blockIdx.y : cols.xb0 + ((int)blockIdx.y - na);
@@ -454,7 +456,7 @@ __global__ void __launch_bounds__(TPB) k_step_fused(const double* __restrict__ A
     }
     if (!interior && BC == BC_THERMAL && (y < 3 || y >= g.ly - 3)) thermal_wall(f, y < 3 ? 0 : 1);
   }
-  collide_any<COLL>(f, omega, one_m_omega);
+  collide_any<COLL>(f, r);
   store_site(B, g, ix, y, f);
   if (h.dstL != nullptr && ix < 2 * H) store_site(h.dstL, g, ix + g.lx, y, f);
   if (h.dstR != nullptr && ix >= g.lx) store_site(h.dstR, g, ix - g.lx, y, f);
@@ -462,25 +464,24 @@ __global__ void __launch_bounds__(TPB) k_step_fused(const double* __restrict__ A
 }
 
 template <int COLL>
-void launch_fused_bc(const Geo& g, const double* A, double* B, int bc, double omega, Cols cols,
+void launch_fused_bc(const Geo& g, const double* A, double* B, int bc, const Relax& r, Cols cols,
                      const Halo& h, dim3 grid, cudaStream_t s) {
-  const double om1 = 1.0 - omega;
   switch (bc) {
-    case BC_THERMAL: k_step_fused<BC_THERMAL, COLL><<<grid, TPB, 0, s>>>(A, B, g, cols, omega, om1, h); break;
-    case BC_ADIABATIC: k_step_fused<BC_ADIABATIC, COLL><<<grid, TPB, 0, s>>>(A, B, g, cols, omega, om1, h); break;
-    default: k_step_fused<BC_PERIODIC, COLL><<<grid, TPB, 0, s>>>(A, B, g, cols, omega, om1, h); break;
+    case BC_THERMAL: k_step_fused<BC_THERMAL, COLL><<<grid, TPB, 0, s>>>(A, B, g, cols, r, h); break;
+    case BC_ADIABATIC: k_step_fused<BC_ADIABATIC, COLL><<<grid, TPB, 0, s>>>(A, B, g, cols, r, h); break;
+    default: k_step_fused<BC_PERIODIC, COLL><<<grid, TPB, 0, s>>>(A, B, g, cols, r, h); break;
   }
 }
 
 cudaError_t launch_step_fused(const Geo& g, const double* A, double* B, int bc, int coll,
-                              double omega, Cols cols, const Halo& h, cudaStream_t s) {
+                              const Relax& r, Cols cols, const Halo& h, cudaStream_t s) {
   const int n = cols.count();
   if (n <= 0) return cudaSuccess;
   dim3 grid((g.ly + TPB - 1) / TPB, n);
   if (coll == COLL_REGULARIZED)
-    launch_fused_bc<COLL_REGULARIZED>(g, A, B, bc, omega, cols, h, grid, s);
+    launch_fused_bc<COLL_REGULARIZED>(g, A, B, bc, r, cols, h, grid, s);
   else
-    launch_fused_bc<COLL_BGK>(g, A, B, bc, omega, cols, h, grid, s);
+    launch_fused_bc<COLL_BGK>(g, A, B, bc, r, cols, h, grid, s);
   return cudaGetLastError();
 }
 

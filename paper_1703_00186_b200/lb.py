@@ -42,7 +42,7 @@ class lb_params(ctypes.Structure):
     _fields_ = [("lx_total", ctypes.c_int), ("ly", ctypes.c_int), ("tau", ctypes.c_double),
                 ("dt", ctypes.c_double), ("t_bottom", ctypes.c_double), ("t_top", ctypes.c_double),
                 ("bc_y", ctypes.c_int), ("mode", ctypes.c_int), ("overlap", ctypes.c_int),
-                ("collision", ctypes.c_int)]
+                ("collision", ctypes.c_int), ("gx", ctypes.c_double), ("gy", ctypes.c_double)]
 
 
 class lb_dist(ctypes.Structure):
@@ -155,14 +155,15 @@ def kwall(t_wall: float) -> np.ndarray:
 
 
 def make_params(lx_total, ly, tau=0.8, dt=1.0, t_bottom=None, t_top=None, bc_y="thermal",
-                mode="fused", overlap=False, collision="bgk") -> lb_params:
+                mode="fused", overlap=False, collision="bgk", gravity=(0.0, 0.0)) -> lb_params:
     T0 = t0()
     return lb_params(int(lx_total), int(ly), float(tau), float(dt),
                      float(1.05 * T0 if t_bottom is None else t_bottom),
                      float(0.95 * T0 if t_top is None else t_top),
                      BC[bc_y] if isinstance(bc_y, str) else int(bc_y),
                      MODE[mode] if isinstance(mode, str) else int(mode), int(bool(overlap)),
-                     COLLISION[collision] if isinstance(collision, str) else int(collision))
+                     COLLISION[collision] if isinstance(collision, str) else int(collision),
+                     float(gravity[0]), float(gravity[1]))
 
 
 def query_layout(params: lb_params, rank: int = 0, nranks: int = 1) -> lb_layout:
@@ -193,11 +194,12 @@ class Lattice:
 
     def __init__(self, lx_total, ly, tau=0.8, dt=1.0, t_bottom=None, t_top=None, bc_y="thermal",
                  mode="fused", overlap=False, rank=0, nranks=1, nccl_id: bytes | None = None,
-                 device=None, stream=None, collision="bgk"):
+                 device=None, stream=None, collision="bgk", gravity=(0.0, 0.0)):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("paper_1703_00186_b200 needs a CUDA device (no CPU fallback)")
-        self.params = make_params(lx_total, ly, tau, dt, t_bottom, t_top, bc_y, mode, overlap, collision)
+        self.params = make_params(lx_total, ly, tau, dt, t_bottom, t_top, bc_y, mode, overlap, collision,
+                                  gravity)
         self.layout = query_layout(self.params, rank, nranks)
         self.rank, self.nranks = rank, nranks
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)

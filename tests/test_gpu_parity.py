@@ -353,3 +353,44 @@ def test_peer_exchange_ring_equals_single_lattice(lb, nranks, streams, coll):
     assert max_rel(got, o.get_state(0)) < TOL
     for g in ranks:
         g.close()
+
+
+# ------------------------------------------------------------------ body force (NEXT 2)
+
+@pytest.mark.parametrize("mode,coll", [("fused", "bgk"), ("split", "bgk"), ("fused", "regularized")])
+def test_gravity_trajectory_parity(lb, mode, coll):
+    """Rayleigh-Taylor with gravity (shifted equilibrium, reading G7b), 64x32, 10 steps."""
+    lx, ly = 64, 32
+    grav = (0.0, -2e-4)
+    g = lb.Lattice(lx, ly, mode=mode, collision=coll, gravity=grav)
+    o = oracle.Lattice(lx, ly, collision=oracle.REGULARIZED if coll == "regularized" else oracle.BGK,
+                       gravity=grav)
+    fields = lbgen.rt_macro(lx, ly, oracle.t0())
+    g.init_macro(*fields)
+    o.init_macro(*fields)
+    for k in range(10):
+        g.step(1)
+        o.step(1)
+        assert max_rel(g.gather(), o.get_state(0)) < TOL, k
+
+
+def test_gravity_zero_is_bit_identical_to_unforced(lb):
+    lx, ly = 40, 50
+    st = oracle_state(lx, ly, seed=5)
+    a = lb.Lattice(lx, ly)
+    b = lb.Lattice(lx, ly, gravity=(0.0, 0.0))
+    for x in (a, b):
+        x.set_state(st)
+        x.step(4)
+    assert np.array_equal(a.gather(), b.gather())
+
+
+def test_gravity_free_fall_periodic(lb):
+    """Uniform fluid at rest, periodic box: momentum grows as n rho g (closed form)."""
+    lx, ly, n, gy = 16, 24, 30, -1e-4
+    g = lb.Lattice(lx, ly, bc_y="periodic", gravity=(0.0, gy))
+    ones = np.ones((lx, ly))
+    g.init_macro(ones, 0 * ones, 0 * ones, oracle.t0() * ones)
+    g.step(n)
+    inv = g.invariants()
+    assert abs(inv[2] - n * lx * ly * gy) < 1e-10 * abs(n * lx * ly * gy)
