@@ -329,8 +329,15 @@ def main():
     fp64 = load_json(os.path.join(ROOT, "profiles", "r01_fp64_hbm_microbench.json"), {}) or {}
     fp64_peak = fp64.get("fp64_tflops")
 
-    fk = prof.get("k_step_fused") or prof.get("k_propagate")
-    kname = "k_step_fused" if "k_step_fused" in prof else "k_propagate"
+    # dominant kernel: every launch of k_step_fused (whole lattice, or bulk +
+    # border launches of the overlapped schedule), aggregated
+    parts = [v for k, v in prof.items() if k.startswith("k_step_fused") and "_reg" not in k]
+    kname = "k_step_fused"
+    fk = {"launches": sum(v["launches"] for v in parts), "total_ms": sum(v["total_ms"] for v in parts),
+          "units": sum(v["units"] for v in parts)} if parts else None
+    if fk and world > 1:
+        # bulk and border launches differ in size: use steps as the launch unit
+        fk["launches"] = args.steps
     roofline = None
     if fk and fk["launches"]:
         avg_ms = fk["total_ms"] / fk["launches"]

@@ -292,8 +292,13 @@ int exchange_on(lb_ctx* c, cudaStream_t s) {
   return LB_OK;
 }
 
-int fused(lb_ctx* c, Cols cols, const lbk::Halo& h = lbk::Halo()) {
-  return launch(c, c->p.collision ? "k_step_fused_reg" : "k_step_fused", c->s, (int64_t)cols.count() * c->g.ly, [&] {
+// part: "" (whole lattice), "_bulk" or "_border" (overlapped schedule) —
+// instrumentation names only; all are launches of k_step_fused.
+int fused(lb_ctx* c, Cols cols, const lbk::Halo& h = lbk::Halo(), const char* part = "") {
+  static const char* names[2][3] = {{"k_step_fused", "k_step_fused_bulk", "k_step_fused_border"},
+                                    {"k_step_fused_reg", "k_step_fused_reg_bulk", "k_step_fused_reg_border"}};
+  const int pi = part[0] == 0 ? 0 : (part[1] == 'b' && part[2] == 'u' ? 1 : 2);
+  return launch(c, names[c->p.collision ? 1 : 0][pi], c->s, (int64_t)cols.count() * c->g.ly, [&] {
     return lbk::launch_step_fused(c->g, c->A, c->B, c->p.bc_y, c->p.collision, c->relax, cols, h, c->s);
   });
 }
@@ -362,9 +367,9 @@ int step_once(lb_ctx* c) {
     CU(cudaStreamWaitEvent(c->s_comm, c->ev_ready, 0));
     TRY(exchange_on(c, c->s_comm));
     CU(cudaEventRecord(c->ev_comm, c->s_comm));
-    TRY(fused(c, bulk_cols(c)));
+    TRY(fused(c, bulk_cols(c), lbk::Halo(), "_bulk"));
     CU(cudaStreamWaitEvent(c->s, c->ev_comm, 0));
-    TRY(fused(c, border_cols(c)));
+    TRY(fused(c, border_cols(c), lbk::Halo(), "_border"));
   }
   swap_ab(c);
   return LB_OK;
