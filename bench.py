@@ -250,6 +250,7 @@ def main():
 
     import lbgen
     import paper_1703_00186_b200 as lb
+    from paper_1703_00186_b200 import perfmodel as pm
 
     # LB_BENCH_SAME_GPU=1 (test only): all ranks on cuda:0, gloo process group,
     # no NCCL communicator, peer transport -- exercises the N > 1 code path of
@@ -318,7 +319,7 @@ def main():
     prof = g.profile_read()
     g.profile(False)
     sites_all = lx_total * ly
-    value = sites_all * args.steps / (ms * 1e-3) / 1e6
+    value = pm.mlups(sites_all * args.steps, ms * 1e-3)   # Table 1 convention (tests/test_metrics.py)
 
     peaks = load_json(os.path.join(ROOT, "MEASURED_PEAKS.json"), {}) or {}
     hbm_peak = peaks.get("hbm_gbs")
@@ -342,7 +343,7 @@ def main():
     if fk and fk["launches"]:
         avg_ms = fk["total_ms"] / fk["launches"]
         bytes_per_launch = BYTES_PER_SITE * fk["units"] / fk["launches"]
-        achieved = bytes_per_launch / (avg_ms * 1e-3) / 1e9
+        achieved = pm.gbs(fk["units"] / fk["launches"], avg_ms * 1e-3)   # sites x 592 B / t
         kn = ncu.get("kernels", {}).get(kname, {})
         traffic = kn.get("dram_bytes_per_site")
         roofline = {"kernel": kname, "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak,

@@ -71,3 +71,17 @@ def exchange_gamma(bytes_per_row: float, link_bytes_per_s: float) -> float:
     3 columns x 37 populations x 8 B per row; both directions and both
     neighbours are in flight at once, so the rank's egress is 2 x that."""
     return bytes_per_row / link_bytes_per_s
+
+
+# ---- metric conventions (Table 1 / Table 3 of the paper, P:623-654, P:695-710) ----
+BYTES_PER_SITE = 592  # 37 fp64 reads + 37 fp64 writes per site and step
+
+
+def gbs(sites: float, seconds: float, bytes_per_site: float = BYTES_PER_SITE) -> float:
+    """Effective bandwidth of a step kernel: sites * 592 B / t."""
+    return sites * bytes_per_site / seconds / 1e9
+
+
+def mlups(sites: float, seconds: float) -> float:
+    """Millions of lattice-site updates per second."""
+    return sites / seconds / 1e6
