@@ -6,7 +6,8 @@
 
 A "step" is one full D2Q37 time step (pbc -> propagate -> bc -> collide, fused
 pull kernel) over the whole lattice.  N = 1: config #2 of BASELINE.json, the
-1920x2048 lattice; N > 1 (torchrun, one rank per GPU, NCCL ring exchange):
+1920x2048 lattice; N > 1 (torchrun, one rank per GPU; halo exchange by peer
+stores fused into the step kernel over CUDA-IPC/NVLink, or --transport nccl):
 weak scaling with 1920x2048 per GPU (global lattice 1920N x 2048).  value =
 lattice sites of all ranks x K / max-over-ranks device time (MLUPS).
 
@@ -379,6 +380,7 @@ def main():
         host_in.numpy()[:] = st0.reshape(-1)
         del st0
         k_e2e = max(10, min(args.steps, 100))
+        g.monitor(True)   # per-step invariants reduced inside the step kernel (lb_monitor)
         barrier()
         torch.cuda.synchronize()
         t = time.perf_counter()
@@ -396,7 +398,8 @@ def main():
                        "h2d_bytes_per_step": state_bytes / k_e2e,
                        "d2h_bytes_per_step": (state_bytes + 5 * 8 * k_e2e) / k_e2e,
                        "steps": k_e2e, "mode": args.mode,
-                       "timed": "lb_set_state(pinned host) + K x (lb_step(1) + lb_invariants -> host) + lb_gather(pinned host)"}
+                       "timed": "lb_set_state(pinned host) + K x (lb_step(1) with fused monitors + "
+                                "lb_invariants -> host) + lb_gather(pinned host)"}
         del host_in, host_out
         # ---- per-kernel passes (N = 1): split BGK (propagate GB/s, collide FP64 %),
         #      fused and split regularised collide (NEXT 1)

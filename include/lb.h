@@ -272,6 +272,14 @@ int lb_invariants(lb_ctx* ctx, double* out);
 
 int lb_sync(lb_ctx* ctx);
 
+/* Fused monitors.  enable != 0: every fused step also reduces, per block, the
+ * invariants of the state it writes (rho, j, E sums and min rho of its sites)
+ * into a small per-block array, and lb_invariants after such a step sums
+ * those partials (one tiny kernel) instead of re-reading the lattice (296
+ * B/site).  Values agree with the full pass to rounding (different summation
+ * tree).  Allocates lx*ceil(ly/128)*40 B on first enable. */
+int lb_monitor(lb_ctx* ctx, int enable);
+
 /* ---- instrumentation ----------------------------------------------------- */
 
 /* enable != 0: bracket every kernel launch with CUDA events on the stream it

@@ -132,6 +132,9 @@ struct lb_ctx {
   bool peers_on = false;      // peer-store exchange (lb_set_peers)
   lb_peers peers{};
   uint64_t peer_step = 0;     // steps completed since lb_set_peers
+  bool mon_on = false;        // fused monitors (lb_monitor)
+  bool mon_valid = false;     // d_mon describes the current A
+  double* d_mon = nullptr;    // monitor_slots x 5 partials
   double omega = 1.0;
   lbd::Relax relax{};
   int64_t launches = 0;
@@ -299,7 +302,8 @@ int fused(lb_ctx* c, Cols cols, const lbk::Halo& h = lbk::Halo(), const char* pa
                                     {"k_step_fused_reg", "k_step_fused_reg_bulk", "k_step_fused_reg_border"}};
   const int pi = part[0] == 0 ? 0 : (part[1] == 'b' && part[2] == 'u' ? 1 : 2);
   return launch(c, names[c->p.collision ? 1 : 0][pi], c->s, (int64_t)cols.count() * c->g.ly, [&] {
-    return lbk::launch_step_fused(c->g, c->A, c->B, c->p.bc_y, c->p.collision, c->relax, cols, h, c->s);
+    return lbk::launch_step_fused(c->g, c->A, c->B, c->p.bc_y, c->p.collision, c->relax, cols, h,
+                                  c->mon_on ? c->d_mon : nullptr, c->s);
   });
 }
 
@@ -307,6 +311,9 @@ void swap_ab(lb_ctx* c) {
   std::swap(c->A, c->B);
   c->par ^= 1;
 }
+
+// after a fused step: the monitor partials describe the new A iff monitors ran
+void fused_step_done(lb_ctx* c) { c->mon_valid = c->mon_on; }
 
 // Peer mode (lb_set_peers): one fused kernel per step whose border blocks
 // wait for both neighbours' previous step, pull their halo from this rank's A
@@ -331,6 +338,7 @@ int step_peer(lb_ctx* c) {
   }));
   swap_ab(c);
   c->halo_fresh = true;
+  fused_step_done(c);
   return LB_OK;
 }
 
@@ -352,6 +360,7 @@ int step_once(lb_ctx* c) {
     TRY(fused(c, all_cols(c), h));
     swap_ab(c);
     c->halo_fresh = true;
+    fused_step_done(c);
     return LB_OK;
   }
   // PERIODIC-Y: the y-halo wrap rewrites rows the bulk reads, so no overlap there
@@ -372,6 +381,7 @@ int step_once(lb_ctx* c) {
     TRY(fused(c, border_cols(c), lbk::Halo(), "_border"));
   }
   swap_ab(c);
+  fused_step_done(c);
   return LB_OK;
 }
 
@@ -540,6 +550,7 @@ void lb_destroy(lb_ctx* c) {
   if (c->ev_comm) cudaEventDestroy(c->ev_comm);
   if (c->s_comm) cudaStreamDestroy(c->s_comm);
   if (c->d_part) cudaFree(c->d_part);
+  if (c->d_mon) cudaFree(c->d_mon);
   if (c->h_pin) cudaFreeHost(c->h_pin);
   delete c;
 }
@@ -573,6 +584,7 @@ int lb_init_macro(lb_ctx* c, const double* rho, const double* ux, const double* 
     }
   }
   c->halo_fresh = false;
+  c->mon_valid = false;
   TRY(launch(c, "k_init_macro", c->s, n, [&] {
     return lbk::launch_init_macro(c->g, c->A, dev[0], dev[1], dev[2], dev[3], c->s);
   }));
@@ -590,6 +602,7 @@ int lb_set_state(lb_ctx* c, const double* canon, int on_device) {
     src = c->B;
   }
   c->halo_fresh = false;
+  c->mon_valid = false;
   TRY(launch(c, "k_canon_to_internal", c->s, c->L.sites, [&] {
     return lbk::launch_canon_to_internal(c->g, src, c->A, c->s);
   }));
@@ -642,6 +655,7 @@ int lb_collide(lb_ctx* c) {
   swap_ab(c);
   c->phase = 0;
   c->halo_fresh = false;
+  c->mon_valid = false;
   return LB_OK;
 }
 
@@ -713,9 +727,15 @@ int lb_invariants(lb_ctx* c, double* out) {
   TRY(check_boundary(c, "lb_invariants"));
   if (!out) return fail(LB_EINVAL, "out is NULL");
   double* res = c->d_part + lbk::invariants_scratch(c->g);
-  TRY(launch(c, "k_invariants", c->s, c->L.sites, [&] {
-    return lbk::launch_invariants(c->g, c->A, c->d_part, res, c->s);
-  }));
+  if (c->mon_valid) {
+    TRY(launch(c, "k_monitor_reduce", c->s, 0, [&] {
+      return lbk::launch_monitor_reduce(c->d_mon, (int64_t)lbk::monitor_slots(c->g), res, c->s);
+    }));
+  } else {
+    TRY(launch(c, "k_invariants", c->s, c->L.sites, [&] {
+      return lbk::launch_invariants(c->g, c->A, c->d_part, res, c->s);
+    }));
+  }
   if (c->comm) {
     NC(ncclGroupStart());
     NC(ncclAllReduce(res, res, 4, ncclDouble, ncclSum, c->comm, c->s));
@@ -746,6 +766,17 @@ int lb_set_peers(lb_ctx* c, const lb_peers* p) {
   c->halo_fresh = false;
   CU(cudaMemsetAsync(p->my_done, 0, sizeof(uint64_t), c->s));
   CU(cudaStreamSynchronize(c->s));
+  return LB_OK;
+}
+
+int lb_monitor(lb_ctx* c, int enable) {
+  if (!c) return fail(LB_EINVAL, "ctx is NULL");
+  if (enable && !c->d_mon) {
+    if (cudaMalloc(&c->d_mon, lbk::monitor_slots(c->g) * 5 * sizeof(double)) != cudaSuccess)
+      return fail(LB_ENOMEM, "monitor allocation failed");
+  }
+  c->mon_on = enable != 0;
+  c->mon_valid = false;
   return LB_OK;
 }
 

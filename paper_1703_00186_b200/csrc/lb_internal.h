@@ -46,8 +46,11 @@ struct Halo {
   const unsigned long long* waitR = nullptr;
   unsigned long long wait_val = 0;
 };
+// mon != nullptr: fused monitors, monitor_slots(g) x 5 doubles of per-block partials
 cudaError_t launch_step_fused(const Geo& g, const double* A, double* B, int bc, int coll,
-                              const lbd::Relax& r, Cols cols, const Halo& h, cudaStream_t s);
+                              const lbd::Relax& r, Cols cols, const Halo& h, double* mon, cudaStream_t s);
+size_t monitor_slots(const Geo& g);
+cudaError_t launch_monitor_reduce(const double* mon, int64_t nslots, double* out, cudaStream_t s);
 cudaError_t launch_signal(unsigned long long* done, unsigned long long v, cudaStream_t s);
 cudaError_t launch_peer_pull(const Geo& g, double* A, const double* left_A, const double* right_A,
                              cudaStream_t s);

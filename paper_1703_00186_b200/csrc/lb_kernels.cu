@@ -424,10 +424,56 @@ __device__ __forceinline__ void gather_cg(const double* A, const Geo& g, int ix,
   }
 }
 
-template <int BC, int COLL>
+// Per-site contributions to the invariants: rho, j_x, j_y, E = 1/2 sum |c|^2 f.
+__device__ __forceinline__ void site_invariants(const double (&f)[Q], double (&v)[4]) {
+  double rho = 0.0, jx = 0.0, jy = 0.0, e = 0.0;
+#pragma unroll
+  for (int l = 0; l < Q; ++l) {
+    rho = __dadd_rn(rho, f[l]);
+    jx = __fma_rn((double)CX(l), f[l], jx);
+    jy = __fma_rn((double)CY(l), f[l], jy);
+    e = __fma_rn(0.5 * (double)c2(l), f[l], e);
+  }
+  v[0] = rho;
+  v[1] = jx;
+  v[2] = jy;
+  v[3] = e;
+}
+
+// Fixed-order (deterministic) reduction of 4 sums + 1 min over a TPB block;
+// the result is valid in thread 0.
+__device__ __forceinline__ void block_sum4_min1(double (&v)[5]) {
+  __shared__ double sm[TPB / 32][5];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = __dadd_rn(v[k], __shfl_xor_sync(0xffffffffu, v[k], o));
+    v[4] = fmin(v[4], __shfl_xor_sync(0xffffffffu, v[4], o));
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0)
+#pragma unroll
+    for (int k = 0; k < 5; ++k) sm[w][k] = v[k];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < 5; ++k) v[k] = sm[0][k];
+#pragma unroll
+    for (int ww = 1; ww < TPB / 32; ++ww) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) v[k] = __dadd_rn(v[k], sm[ww][k]);
+      v[4] = fmin(v[4], sm[ww][4]);
+    }
+  }
+}
+
+// MON: fused monitors — each block also reduces the invariants of the state it
+// writes (post-collision rho, j, E and min rho of its 128 sites) into its slot
+// mon[(ix - 3) * nblk_y + blockIdx.x][5]; lb_invariants then only sums slots.
+template <int BC, int COLL, bool MON>
 __global__ void __launch_bounds__(TPB, BC == BC_PERIODIC ? 3 : 4) k_step_fused(const double* __restrict__ A,
                                                     double* __restrict__ B, Geo g, Cols cols,
-                                                    Relax r, Halo h) {
+                                                    Relax r, Halo h, double* __restrict__ mon) {
   const int y = blockIdx.x * TPB + threadIdx.x;
   const int na = cols.xa1 - cols.xa0;
   const int ix = (int)blockIdx.y < na ? cols.xa0 + (int)blockIdx.y : cols.xb0 + ((int)blockIdx.y - na);
@@ -439,51 +485,77 @@ __global__ void __launch_bounds__(TPB, BC == BC_PERIODIC ? 3 : 4) k_step_fused(c
     }
     __syncthreads();
   }
-  if (y >= g.ly) return;
+  const bool valid = y < g.ly;
+  if (!MON && !valid) return;
   double f[Q];
-  if (BC == BC_PERIODIC) {
-    gather<false>(A, g, ix, y, f);
-  } else {
-    const int wy0 = blockIdx.x * TPB + (threadIdx.x & ~31);
-    const bool interior = (wy0 >= 3) && (wy0 + 32 <= g.ly - 3);
-    if (peer_wait) {
-      if (interior) gather_cg<false>(A, g, ix, y, f);
-      else gather_cg<true>(A, g, ix, y, f);
-    } else if (interior) {
+  if (valid) {
+    if (BC == BC_PERIODIC) {
       gather<false>(A, g, ix, y, f);
     } else {
-      gather<true>(A, g, ix, y, f);
+      const int wy0 = blockIdx.x * TPB + (threadIdx.x & ~31);
+      const bool interior = (wy0 >= 3) && (wy0 + 32 <= g.ly - 3);
+      if (peer_wait) {
+        if (interior) gather_cg<false>(A, g, ix, y, f);
+        else gather_cg<true>(A, g, ix, y, f);
+      } else if (interior) {
+        gather<false>(A, g, ix, y, f);
+      } else {
+        gather<true>(A, g, ix, y, f);
+      }
+      if (!interior && BC == BC_THERMAL && (y < 3 || y >= g.ly - 3)) thermal_wall(f, y < 3 ? 0 : 1);
     }
-    if (!interior && BC == BC_THERMAL && (y < 3 || y >= g.ly - 3)) thermal_wall(f, y < 3 ? 0 : 1);
+    collide_any<COLL>(f, r);
+    store_site(B, g, ix, y, f);
+    if (h.dstL != nullptr && ix < 2 * H) store_site(h.dstL, g, ix + g.lx, y, f);
+    if (h.dstR != nullptr && ix >= g.lx) store_site(h.dstR, g, ix - g.lx, y, f);
   }
-  collide_any<COLL>(f, r);
-  store_site(B, g, ix, y, f);
-  if (h.dstL != nullptr && ix < 2 * H) store_site(h.dstL, g, ix + g.lx, y, f);
-  if (h.dstR != nullptr && ix >= g.lx) store_site(h.dstR, g, ix - g.lx, y, f);
+  if (MON) {
+    double v[5] = {0.0, 0.0, 0.0, 0.0, INFINITY};
+    if (valid) {
+      double s[4];
+      site_invariants(f, s);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) v[k] = s[k];
+      v[4] = (s[0] != s[0]) ? -INFINITY : s[0];
+    }
+    block_sum4_min1(v);
+    if (threadIdx.x == 0) {
+      double* slot = mon + ((int64_t)(ix - H) * gridDim.x + blockIdx.x) * 5;
+#pragma unroll
+      for (int k = 0; k < 5; ++k) slot[k] = v[k];
+    }
+  }
   if (peer_wait) __threadfence_system();  // remote halo stores performed before the step signal
 }
 
-template <int COLL>
+template <int COLL, bool MON>
 void launch_fused_bc(const Geo& g, const double* A, double* B, int bc, const Relax& r, Cols cols,
-                     const Halo& h, dim3 grid, cudaStream_t s) {
+                     const Halo& h, double* mon, dim3 grid, cudaStream_t s) {
   switch (bc) {
-    case BC_THERMAL: k_step_fused<BC_THERMAL, COLL><<<grid, TPB, 0, s>>>(A, B, g, cols, r, h); break;
-    case BC_ADIABATIC: k_step_fused<BC_ADIABATIC, COLL><<<grid, TPB, 0, s>>>(A, B, g, cols, r, h); break;
-    default: k_step_fused<BC_PERIODIC, COLL><<<grid, TPB, 0, s>>>(A, B, g, cols, r, h); break;
+    case BC_THERMAL: k_step_fused<BC_THERMAL, COLL, MON><<<grid, TPB, 0, s>>>(A, B, g, cols, r, h, mon); break;
+    case BC_ADIABATIC: k_step_fused<BC_ADIABATIC, COLL, MON><<<grid, TPB, 0, s>>>(A, B, g, cols, r, h, mon); break;
+    default: k_step_fused<BC_PERIODIC, COLL, MON><<<grid, TPB, 0, s>>>(A, B, g, cols, r, h, mon); break;
   }
 }
 
+size_t monitor_slots(const Geo& g) { return (size_t)g.lx * ((g.ly + TPB - 1) / TPB); }
+
 cudaError_t launch_step_fused(const Geo& g, const double* A, double* B, int bc, int coll,
-                              const Relax& r, Cols cols, const Halo& h, cudaStream_t s) {
+                              const Relax& r, Cols cols, const Halo& h, double* mon, cudaStream_t s) {
   const int n = cols.count();
   if (n <= 0) return cudaSuccess;
   dim3 grid((g.ly + TPB - 1) / TPB, n);
-  if (coll == COLL_REGULARIZED)
-    launch_fused_bc<COLL_REGULARIZED>(g, A, B, bc, r, cols, h, grid, s);
-  else
-    launch_fused_bc<COLL_BGK>(g, A, B, bc, r, cols, h, grid, s);
+  if (coll == COLL_REGULARIZED) {
+    if (mon) launch_fused_bc<COLL_REGULARIZED, true>(g, A, B, bc, r, cols, h, mon, grid, s);
+    else launch_fused_bc<COLL_REGULARIZED, false>(g, A, B, bc, r, cols, h, mon, grid, s);
+  } else {
+    if (mon) launch_fused_bc<COLL_BGK, true>(g, A, B, bc, r, cols, h, mon, grid, s);
+    else launch_fused_bc<COLL_BGK, false>(g, A, B, bc, r, cols, h, mon, grid, s);
+  }
   return cudaGetLastError();
 }
+
+cudaError_t launch_monitor_reduce(const double* mon, int64_t nslots, double* out, cudaStream_t s);
 
 // Step signal of peer mode: this rank's counter := v (system-scope release),
 // after the fused kernel (stream order) and its border blocks' system fences.
@@ -649,6 +721,11 @@ cudaError_t launch_invariants(const Geo& g, const double* A, double* partials, d
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   k_invariants_final<<<1, RED_TPB, 0, s>>>(partials, g.lx, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_monitor_reduce(const double* mon, int64_t nslots, double* out, cudaStream_t s) {
+  k_invariants_final<<<1, RED_TPB, 0, s>>>(mon, (int)nslots, out);
   return cudaGetLastError();
 }
 

@@ -29,7 +29,8 @@ EXPORTS = ["lb_query_layout", "lb_exchange_plan", "lb_constants", "lb_kwall", "l
            "lb_strerror", "lb_init", "lb_destroy", "lb_get_layout", "lb_set_stream", "lb_init_macro",
            "lb_set_state", "lb_exchange", "lb_propagate", "lb_bc", "lb_collide", "lb_step",
            "lb_gather", "lb_peek", "lb_invariants", "lb_sync", "lb_profile_enable",
-           "lb_profile_reset", "lb_profile_read", "lb_launch_count", "lb_set_peers"]
+           "lb_profile_reset", "lb_profile_read", "lb_launch_count", "lb_set_peers",
+           "lb_monitor"]
 
 
 class LBError(RuntimeError):
@@ -113,6 +114,7 @@ def lib():
         "lb_profile_read": (i, [vp, p(lb_kprof), i, p(i)]),
         "lb_launch_count": (ctypes.c_int64, [vp]),
         "lb_set_peers": (i, [vp, p(lb_peers)]),
+        "lb_monitor": (i, [vp, i]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -380,6 +382,10 @@ class Lattice:
         P.right_buf[0], P.right_buf[1] = right_bufs
         P.left_done, P.right_done, P.my_done = left_done, right_done, my_done
         _check(lib().lb_set_peers(self._ctx, ctypes.byref(P)))
+
+    def monitor(self, enable: bool = True):
+        """Fused monitors: invariants reduced inside the step kernel (lb_monitor)."""
+        _check(lib().lb_monitor(self._ctx, int(enable)))
 
     def launch_count(self) -> int:
         return int(lib().lb_launch_count(self._ctx))

@@ -394,3 +394,32 @@ def test_gravity_free_fall_periodic(lb):
     g.step(n)
     inv = g.invariants()
     assert abs(inv[2] - n * lx * ly * gy) < 1e-10 * abs(n * lx * ly * gy)
+
+
+# ------------------------------------------------------------------ fused monitors
+
+@pytest.mark.parametrize("overlap,nccl", [(False, False), (True, True)])
+def test_fused_monitors(lb, overlap, nccl):
+    """Monitored fused steps leave the state bit-identical, and the in-kernel
+    invariants equal the full-pass invariants and the oracle's to rounding."""
+    lx, ly = 50, 131
+    st = oracle_state(lx, ly, seed=12)
+    # one fresh NCCL unique id per communicator
+    a = lb.Lattice(lx, ly, overlap=overlap, nccl_id=lb.nccl_unique_id() if nccl else None)
+    b = lb.Lattice(lx, ly, overlap=overlap, nccl_id=lb.nccl_unique_id() if nccl else None)
+    for x in (a, b):
+        x.set_state(st)
+    b.monitor(True)
+    a.step(3)
+    b.step(3)
+    inv_mon = b.invariants()          # from the per-block partials
+    assert np.array_equal(a.gather(), b.gather())
+    b.monitor(False)
+    inv_full = b.invariants()         # full pass over the lattice
+    assert np.allclose(inv_mon[:4], inv_full[:4], rtol=1e-13, atol=1e-13 * inv_full[0])
+    assert inv_mon[4] == inv_full[4]
+    o = oracle.Lattice(lx, ly)
+    o.set_state(st)
+    o.step(3)
+    ref = o.invariants(0)
+    assert abs(inv_mon[0] - ref[0]) < 1e-13 * ref[0]
