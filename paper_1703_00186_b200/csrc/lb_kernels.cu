@@ -313,40 +313,38 @@ cudaError_t launch_propagate(const Geo& g, const double* A, double* B, cudaStrea
 template <int BC>
 __global__ void __launch_bounds__(TPB) k_bc(const double* __restrict__ A, double* __restrict__ B,
                                             Geo g) {
-  const int t = blockIdx.x * TPB + threadIdx.x;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= g.lx * 6) return;
   const int ix = H + t / 6;
   const int j = t % 6;
   const int y = j < 3 ? j : g.ly - 6 + j;
   double* p = B + (int64_t)ix * g.cs + g.y0 + y;
+  // all 37 values of the site in registers (mirrored ones from A, the rest as
+  // propagated into B), so no load waits on a store to the same address
+  double f[Q];
 #pragma unroll
   for (int l = 0; l < Q; ++l) {
     const int sy = y - CY(l);
-    int ys;
+    int ys = -1;
     if (sy < 0) ys = -1 - sy;
     else if (sy >= g.ly) ys = 2 * g.ly - 1 - sy;
-    else continue;
-    p[(int64_t)l * g.nyp] =
-        A[(int64_t)(ix - CX(l)) * g.cs + (int64_t)refl(l) * g.nyp + g.y0 + ys];
+    f[l] = ys >= 0 ? __ldg(A + (int64_t)(ix - CX(l)) * g.cs + (int64_t)refl(l) * g.nyp + g.y0 + ys)
+                   : p[(int64_t)l * g.nyp];
   }
-  if (BC == BC_THERMAL) {
-    double f[Q];
+  if (BC == BC_THERMAL) thermal_wall(f, j < 3 ? 0 : 1);
 #pragma unroll
-    for (int l = 0; l < Q; ++l) f[l] = p[(int64_t)l * g.nyp];
-    thermal_wall(f, j < 3 ? 0 : 1);
-#pragma unroll
-    for (int l = 0; l < Q; ++l) p[(int64_t)l * g.nyp] = f[l];
-  }
+  for (int l = 0; l < Q; ++l) p[(int64_t)l * g.nyp] = f[l];
 }
 
 cudaError_t launch_bc(const Geo& g, const double* A, double* B, int bc, cudaStream_t s) {
   if (bc == BC_PERIODIC) return cudaSuccess;
   const int n = g.lx * 6;
-  const int blocks = (n + TPB - 1) / TPB;
+  constexpr int BC_TPB = 32;  // few, latency-bound threads: spread them over many SMs
+  const int blocks = (n + BC_TPB - 1) / BC_TPB;
   if (bc == BC_THERMAL)
-    k_bc<BC_THERMAL><<<blocks, TPB, 0, s>>>(A, B, g);
+    k_bc<BC_THERMAL><<<blocks, BC_TPB, 0, s>>>(A, B, g);
   else
-    k_bc<BC_ADIABATIC><<<blocks, TPB, 0, s>>>(A, B, g);
+    k_bc<BC_ADIABATIC><<<blocks, BC_TPB, 0, s>>>(A, B, g);
   return cudaGetLastError();
 }
 

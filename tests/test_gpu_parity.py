@@ -240,6 +240,24 @@ def test_full_size_1920x2048_one_step(lb, overlap):
     assert max_rel(got, ref) < TOL
 
 
+def test_full_size_1920x2048_regularized_gravity_split():
+    """Full config #2 size with the NEXT rows switched on (regularised collide,
+    gravity) in split mode — every per-kernel launch at full size."""
+    import paper_1703_00186_b200 as lbm
+    lx, ly = 1920, 2048
+    grav = (0.0, -1e-5)
+    fields = lbgen.rt_macro(lx, ly, oracle.t0())
+    g = lbm.Lattice(lx, ly, mode="split", collision="regularized", gravity=grav)
+    g.init_macro(*fields)
+    g.step(1)
+    got = g.gather()
+    del g
+    o = oracle.Lattice(lx, ly, collision=oracle.REGULARIZED, gravity=grav)
+    o.init_macro(*fields)
+    o.step(1)
+    assert max_rel(got, o.get_state(0)) < TOL
+
+
 # ------------------------------------------------------------------ NCCL transport on one GPU
 
 @pytest.mark.parametrize("bc,mode,overlap", [("thermal", "fused", True), ("thermal", "fused", False),
