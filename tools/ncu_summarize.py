@@ -24,9 +24,12 @@ for r in rows:
     name = d["Kernel Name"].split("(")[0].replace("void ", "")
     base = name.split("<")[0]
     targs = name[len(base):].strip("<>").replace(" ", "").split(",") if "<" in name else []
-    # collision kind is the last template argument of k_step_fused<BC, COLL> / k_collide<COLL>
-    if base in ("k_step_fused", "k_collide") and targs and targs[-1] == "1":
+    # collision kind: k_step_fused<BC, COLL, MON> / k_collide<COLL>
+    coll_arg = {"k_step_fused": 1, "k_collide": 0}.get(base)
+    if coll_arg is not None and len(targs) > coll_arg and targs[coll_arg] == "1":
         base += "_reg"
+    if base.startswith("k_step_fused") and len(targs) > 2 and targs[2] in ("1", "true"):
+        base += "_mon"
     try:
         v = float(d["Metric Value"].replace(",", ""))
     except ValueError:
