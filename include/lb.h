@@ -70,7 +70,8 @@ enum lb_status {
   LB_ECUDA = 3,      /* CUDA runtime / kernel error                          */
   LB_ENCCL = 4,      /* NCCL error                                           */
   LB_ENONPHYS = 5,   /* NaN or rho <= 0 detected by lb_invariants            */
-  LB_ENOMEM = 6      /* host or device allocation failed                     */
+  LB_ENOMEM = 6,     /* host or device allocation failed                     */
+  LB_EPEER = 7       /* peer exchange watchdog: a neighbour never signalled  */
 };
 
 enum lb_bc_y {
@@ -247,7 +248,11 @@ int lb_step(lb_ctx* ctx, int nsteps); /* nsteps full steps in p->mode, with the
  * lx >= 6.  Zeroes *my_done and synchronises.  Collective in effect: every
  * rank calls it, then all ranks barrier before the next lb_step; the first
  * step after it (or after lb_set_state / lb_init_macro, which must likewise be
- * followed by a barrier) fills the halos by reading the neighbours' A. */
+ * followed by a barrier) fills the halos by reading the neighbours' A.
+ * Watchdog: a border block that waits longer than 20 s (env
+ * LB_PEER_TIMEOUT_MS overrides) gives up, flags the context and proceeds, so
+ * a dead neighbour cannot hang the GPU; lb_sync / lb_invariants then return
+ * LB_EPEER and the state is invalid. */
 int lb_set_peers(lb_ctx* ctx, const lb_peers* peers);
 
 /* ---- results ------------------------------------------------------------ */
@@ -262,6 +267,10 @@ int lb_gather(lb_ctx* ctx, double* host_out, int root);
  * canonical local layout [37][Lx][Ly], converted on the host; allowed mid-step
  * (e.g. between lb_propagate and lb_bc).  Synchronising. */
 int lb_peek(lb_ctx* ctx, int which, double* host_out);
+/* Same for this rank's physical columns [x0, x0+ncols) only: host_out is
+ * [37][ncols][Ly] (one contiguous D2H of the column block; used for sampled
+ * checks of lattices too large to gather). */
+int lb_peek_cols(lb_ctx* ctx, int which, int x0, int ncols, double* host_out);
 
 /* Collective (local sums if the context has no NCCL communicator).
  * out[0..3] = global sum over physical sites of rho, j_x, j_y

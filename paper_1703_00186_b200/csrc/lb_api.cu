@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -135,6 +136,8 @@ struct lb_ctx {
   bool mon_on = false;        // fused monitors (lb_monitor)
   bool mon_valid = false;     // d_mon describes the current A
   double* d_mon = nullptr;    // monitor_slots x 5 partials
+  unsigned int* d_status = nullptr;        // peer watchdog flag (device)
+  unsigned long long peer_timeout_ns = 20000000000ull;
   double omega = 1.0;
   lbd::Relax relax{};
   int64_t launches = 0;
@@ -331,6 +334,8 @@ int step_peer(lb_ctx* c) {
   h.waitL = reinterpret_cast<const unsigned long long*>(P.left_done);
   h.waitR = reinterpret_cast<const unsigned long long*>(P.right_done);
   h.wait_val = c->peer_step;
+  h.status = c->d_status;
+  h.timeout_ns = c->peer_timeout_ns;
   TRY(fused(c, all_cols(c), h));
   c->peer_step += 1;
   TRY(launch(c, "k_signal", c->s, 0, [&] {
@@ -418,6 +423,7 @@ const char* lb_strerror(int s) {
     case LB_ENCCL: return "NCCL error";
     case LB_ENONPHYS: return "non-physical state (NaN or rho <= 0)";
     case LB_ENOMEM: return "out of memory";
+    case LB_EPEER: return "peer exchange timed out";
     default: return "unknown status";
   }
 }
@@ -551,6 +557,7 @@ void lb_destroy(lb_ctx* c) {
   if (c->s_comm) cudaStreamDestroy(c->s_comm);
   if (c->d_part) cudaFree(c->d_part);
   if (c->d_mon) cudaFree(c->d_mon);
+  if (c->d_status) cudaFree(c->d_status);
   if (c->h_pin) cudaFreeHost(c->h_pin);
   delete c;
 }
@@ -666,11 +673,20 @@ int lb_step(lb_ctx* c, int nsteps) {
   return LB_OK;
 }
 
+// Peer-mode watchdog (step_peer): LB_EPEER if a border block gave up waiting.
+static int check_peer_status(lb_ctx* c) {
+  if (!c->d_status) return LB_OK;
+  unsigned int st = 0;
+  CU(cudaMemcpy(&st, c->d_status, sizeof(st), cudaMemcpyDeviceToHost));
+  if (st) return fail(LB_EPEER, "peer exchange timed out: a neighbour did not complete its step");
+  return LB_OK;
+}
+
 int lb_sync(lb_ctx* c) {
   if (!c) return fail(LB_EINVAL, "ctx is NULL");
   CU(cudaStreamSynchronize(c->s));
   CU(cudaStreamSynchronize(c->s_comm));
-  return LB_OK;
+  return check_peer_status(c);
 }
 
 int lb_gather(lb_ctx* c, double* host_out, int root) {
@@ -703,24 +719,30 @@ int lb_gather(lb_ctx* c, double* host_out, int root) {
   return LB_OK;
 }
 
-int lb_peek(lb_ctx* c, int which, double* host_out) {
+int lb_peek_cols(lb_ctx* c, int which, int x0, int ncols, double* host_out) {
   if (!c || !host_out || (which != 0 && which != 1)) return fail(LB_EINVAL, "bad argument");
   const Geo& g = c->g;
+  if (x0 < 0 || ncols < 1 || x0 + ncols > g.lx) return fail(LB_EINVAL, "column range out of bounds");
   std::vector<double> buf;
   try {
-    buf.resize((size_t)c->L.elems);
+    buf.resize((size_t)ncols * g.cs);
   } catch (...) {
     return fail(LB_ENOMEM, "host staging allocation failed");
   }
+  const double* src = (which ? c->B : c->A) + (int64_t)(x0 + 3) * g.cs;  // contiguous column block
   CU(cudaStreamSynchronize(c->s_comm));
-  CU(cudaMemcpyAsync(buf.data(), which ? c->B : c->A, c->L.bytes, cudaMemcpyDeviceToHost, c->s));
+  CU(cudaMemcpyAsync(buf.data(), src, buf.size() * sizeof(double), cudaMemcpyDeviceToHost, c->s));
   CU(cudaStreamSynchronize(c->s));
   for (int l = 0; l < 37; ++l)
-    for (int x = 0; x < g.lx; ++x)
-      std::memcpy(host_out + ((int64_t)l * g.lx + x) * g.ly,
-                  buf.data() + (int64_t)(x + 3) * g.cs + (int64_t)l * g.nyp + g.y0,
-                  sizeof(double) * g.ly);
+    for (int x = 0; x < ncols; ++x)
+      std::memcpy(host_out + ((int64_t)l * ncols + x) * g.ly,
+                  buf.data() + (int64_t)x * g.cs + (int64_t)l * g.nyp + g.y0, sizeof(double) * g.ly);
   return LB_OK;
+}
+
+int lb_peek(lb_ctx* c, int which, double* host_out) {
+  if (!c) return fail(LB_EINVAL, "ctx is NULL");
+  return lb_peek_cols(c, which, 0, c->g.lx, host_out);
 }
 
 int lb_invariants(lb_ctx* c, double* out) {
@@ -744,6 +766,7 @@ int lb_invariants(lb_ctx* c, double* out) {
   }
   CU(cudaMemcpyAsync(c->h_pin, res, 5 * sizeof(double), cudaMemcpyDeviceToHost, c->s));
   CU(cudaStreamSynchronize(c->s));
+  TRY(check_peer_status(c));
   std::memcpy(out, c->h_pin, 5 * sizeof(double));
   for (int k = 0; k < 5; ++k)
     if (std::isnan(out[k])) return fail(LB_ENONPHYS, "NaN in invariants");
@@ -760,6 +783,10 @@ int lb_set_peers(lb_ctx* c, const lb_peers* p) {
   for (int k = 0; k < 2; ++k)
     if (!p->left_buf[k] || !p->right_buf[k]) return fail(LB_EINVAL, "NULL peer buffer");
   if (!p->left_done || !p->right_done || !p->my_done) return fail(LB_EINVAL, "NULL step counter");
+  if (!c->d_status && cudaMalloc(&c->d_status, sizeof(unsigned int)) != cudaSuccess)
+    return fail(LB_ENOMEM, "status allocation failed");
+  CU(cudaMemsetAsync(c->d_status, 0, sizeof(unsigned int), c->s));
+  if (const char* e = std::getenv("LB_PEER_TIMEOUT_MS")) c->peer_timeout_ns = 1000000ull * std::strtoull(e, nullptr, 10);
   c->peers = *p;
   c->peers_on = true;
   c->peer_step = 0;

@@ -45,6 +45,8 @@ struct Halo {
   const unsigned long long* waitL = nullptr;
   const unsigned long long* waitR = nullptr;
   unsigned long long wait_val = 0;
+  unsigned int* status = nullptr;      // set to 1 if a wait timed out (watchdog)
+  unsigned long long timeout_ns = 0;   // 0: wait forever
 };
 // mon != nullptr: fused monitors, monitor_slots(g) x 5 doubles of per-block partials
 cudaError_t launch_step_fused(const Geo& g, const double* A, double* B, int bc, int coll,

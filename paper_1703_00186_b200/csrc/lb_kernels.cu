@@ -403,6 +403,12 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
   return v;
 }
 
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 template <bool MIRROR>
 __device__ __forceinline__ void gather_cg(const double* A, const Geo& g, int ix, int y, double (&f)[Q]) {
   // like gather<MIRROR> but with L2-coherent loads (halo data written by a
@@ -479,7 +485,17 @@ __global__ void __launch_bounds__(TPB, BC == BC_PERIODIC ? 3 : 4) k_step_fused(c
   const bool peer_wait = h.waitL != nullptr && border;
   if (peer_wait) {  // block-uniform
     if (threadIdx.x == 0) {
-      while (ld_acquire_sys(h.waitL) < h.wait_val || ld_acquire_sys(h.waitR) < h.wait_val) __nanosleep(128);
+      // watchdog: a neighbour that never signals (dead rank) must not hang the
+      // GPU — after timeout_ns the block flags *status and proceeds (the step
+      // result is then invalid; the host reports LB_EPEER at the next sync)
+      const unsigned long long t0 = globaltimer_ns();
+      while (ld_acquire_sys(h.waitL) < h.wait_val || ld_acquire_sys(h.waitR) < h.wait_val) {
+        __nanosleep(128);
+        if (h.timeout_ns && globaltimer_ns() - t0 > h.timeout_ns) {
+          atomicExch(h.status, 1u);
+          break;
+        }
+      }
     }
     __syncthreads();
   }

@@ -16,7 +16,7 @@ import numpy as np
 Q = 37
 HALO = 3
 STATUS = {0: "LB_OK", 1: "LB_EINVAL", 2: "LB_ESTATE", 3: "LB_ECUDA", 4: "LB_ENCCL",
-          5: "LB_ENONPHYS", 6: "LB_ENOMEM"}
+          5: "LB_ENONPHYS", 6: "LB_ENOMEM", 7: "LB_EPEER"}
 BC = {"thermal": 0, "adiabatic": 1, "periodic": 2}
 MODE = {"fused": 0, "split": 1}
 COLLISION = {"bgk": 0, "regularized": 1}
@@ -30,7 +30,7 @@ EXPORTS = ["lb_query_layout", "lb_exchange_plan", "lb_constants", "lb_kwall", "l
            "lb_set_state", "lb_exchange", "lb_propagate", "lb_bc", "lb_collide", "lb_step",
            "lb_gather", "lb_peek", "lb_invariants", "lb_sync", "lb_profile_enable",
            "lb_profile_reset", "lb_profile_read", "lb_launch_count", "lb_set_peers",
-           "lb_monitor"]
+           "lb_monitor", "lb_peek_cols"]
 
 
 class LBError(RuntimeError):
@@ -108,6 +108,7 @@ def lib():
         "lb_collide": (i, [vp]), "lb_step": (i, [vp, i]),
         "lb_gather": (i, [vp, vp, i]),
         "lb_peek": (i, [vp, i, vp]),
+        "lb_peek_cols": (i, [vp, i, i, i, vp]),
         "lb_invariants": (i, [vp, vp]),
         "lb_sync": (i, [vp]),
         "lb_profile_enable": (i, [vp, i]), "lb_profile_reset": (i, [vp]),
@@ -307,6 +308,12 @@ class Lattice:
     def peek(self, which: int = 0) -> np.ndarray:
         out = np.empty((Q, self.lx, self.ly))
         _check(lib().lb_peek(self._ctx, which, _dptr(out)))
+        return out
+
+    def peek_cols(self, x0: int, ncols: int, which: int = 0) -> np.ndarray:
+        """Local physical columns [x0, x0+ncols) of A (0) or B (1): [37][ncols][ly]."""
+        out = np.empty((Q, ncols, self.ly))
+        _check(lib().lb_peek_cols(self._ctx, which, int(x0), int(ncols), _dptr(out)))
         return out
 
     def invariants(self) -> np.ndarray:

@@ -1,0 +1,64 @@
+"""Full BASELINE sizes beyond config #2, in the launch configuration bench.py
+times, checked on SAMPLED columns: for a column x the step result depends only
+on columns x-3..x+3 of the previous state, so the oracle steps that 7-column
+window (any halo) and its centre column must match the GPU's column x.
+Also the peer-exchange watchdog."""
+import numpy as np
+import pytest
+
+import lbgen
+import oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def lb():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1703_00186_b200 as m
+    return m
+
+
+def window(g, x, lx):
+    cols = [(x + d) % lx for d in range(-3, 4)]
+    return np.concatenate([g.peek_cols(c, 1) for c in cols], axis=1)
+
+
+@pytest.mark.parametrize("lx,ly,coll", [(8192, 8192, "bgk"), (4096, 8192, "regularized")])
+def test_sampled_columns_full_size(lb, lx, ly, coll):
+    """BASELINE configs #3 (8192x8192, N=1) and #4 (4096x8192 per GPU)."""
+    g = lb.Lattice(lx, ly, collision=coll)
+    g.init_macro(*lbgen.rt_macro(lx, ly, lb.t0()))
+    g.step(2)
+    samples = [0, 1, 2, 3, lx // 2 + 1, lx - 4, lx - 3, lx - 2, lx - 1]
+    wins = {x: window(g, x, lx) for x in samples}
+    g.step(1)
+    for x in samples:
+        got = g.peek_cols(x, 1)[:, 0, :]
+        o = oracle.Lattice(7, ly, collision=oracle.REGULARIZED if coll == "regularized" else oracle.BGK)
+        o.set_state(wins[x])
+        o.step(1)
+        ref = o.get_state(0)[:, 3, :]
+        err = float(np.max(np.abs(got - ref) / np.abs(ref)))
+        assert err < 1e-12, (x, err)
+    g.close()
+
+
+def test_peer_watchdog_reports_dead_neighbour(lb, monkeypatch):
+    """A rank whose neighbour never steps must not hang: the border blocks give
+    up after LB_PEER_TIMEOUT_MS and lb_sync returns LB_EPEER."""
+    monkeypatch.setenv("LB_PEER_TIMEOUT_MS", "200")
+    lx, ly = 16, 40
+    r = [lb.Lattice(2 * lx, ly, rank=k, nranks=2) for k in range(2)]
+    for k, x in enumerate(r):
+        x.init_macro(*lbgen.rt_macro(2 * lx, ly, lb.t0(), x0=k * lx, lx=lx))
+    r[0].set_peers(r[1], r[1])
+    r[1].set_peers(r[0], r[0])
+    r[0].step(2)          # needs r[1]'s step 1, which never comes
+    with pytest.raises(lb.LBError) as ei:
+        r[0].sync()
+    assert ei.value.status == 7
+    for x in r:
+        x.close()
