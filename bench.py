@@ -184,8 +184,10 @@ def kernel_passes(lb, lx_total, ly, fields, hbm_peak, fp64_peak, ncu, nsteps=10)
     """Per-kernel CUDA-event times of split BGK, fused regularised and split
     regularised steps on the same workload (library instrumentation)."""
     kern = {}
-    for mode, coll in (("split", "bgk"), ("fused", "regularized"), ("split", "regularized")):
+    for mode, coll, impl in (("split", "bgk", "ldg"), ("split", "bgk", "tma"), ("fused", "regularized", "ldg"),
+                             ("split", "regularized", "ldg")):
         g = lb.Lattice(lx_total, ly, mode=mode, collision=coll)
+        g.set_propagate_impl(impl)
         g.init_macro(*fields)
         g.step(3)
         g.profile(True)
@@ -198,7 +200,7 @@ def kernel_passes(lb, lx_total, ly, fields, hbm_peak, fp64_peak, ncu, nsteps=10)
                 continue
             avg = v["total_ms"] / max(1, v["launches"])
             e = {"avg_ms": avg, "launches": v["launches"]}
-            if k in ("k_propagate", "k_collide", "k_collide_reg", "k_step_fused_reg"):
+            if k in ("k_propagate", "k_propagate_tma", "k_collide", "k_collide_reg", "k_step_fused_reg"):
                 per = BYTES_PER_SITE * v["units"] / v["launches"]
                 e["gbs"] = per / (avg * 1e-3) / 1e9
                 e["hbm_frac"] = e["gbs"] / hbm_peak
@@ -212,7 +214,7 @@ def kernel_passes(lb, lx_total, ly, fields, hbm_peak, fp64_peak, ncu, nsteps=10)
                 e["paper_convention_6500_flop_tflops"] = 6500 * e["mlups"] * 1e6 / 1e12
             kern[k] = e
         step_ms = sum(v["total_ms"] for v in sp.values()) / nsteps
-        kern[f"{mode}_{coll}_step_mlups"] = lx_total * ly / (step_ms * 1e-3) / 1e6
+        kern[f"{mode}_{coll}" + ("_tma" if impl == "tma" else "") + "_step_mlups"] = lx_total * ly / (step_ms * 1e-3) / 1e6
     return kern
 
 

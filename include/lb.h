@@ -281,6 +281,14 @@ int lb_invariants(lb_ctx* ctx, double* out);
 
 int lb_sync(lb_ctx* ctx);
 
+/* Options.  LB_OPT_PROPAGATE_IMPL (lb_propagate, split mode): 1 = TMA-staged
+ * (cp.async.bulk.tensor 3-D loads of the +-3-row windows into shared memory,
+ * 16-byte vector stores; the default when the tensor maps can be encoded),
+ * 0 = register gather with coalesced 8-byte loads, all 37 in flight per
+ * thread.  Both are bit-identical; bench.py reports both. */
+enum lb_option { LB_OPT_PROPAGATE_IMPL = 0 };
+int lb_set_option(lb_ctx* ctx, int option, int value);
+
 /* Fused monitors.  enable != 0: every fused step also reduces, per block, the
  * invariants of the state it writes (rho, j, E sums and min rho of its sites)
  * into a small per-block array, and lb_invariants after such a step sums

@@ -30,7 +30,7 @@ EXPORTS = ["lb_query_layout", "lb_exchange_plan", "lb_constants", "lb_kwall", "l
            "lb_set_state", "lb_exchange", "lb_propagate", "lb_bc", "lb_collide", "lb_step",
            "lb_gather", "lb_peek", "lb_invariants", "lb_sync", "lb_profile_enable",
            "lb_profile_reset", "lb_profile_read", "lb_launch_count", "lb_set_peers",
-           "lb_monitor", "lb_peek_cols"]
+           "lb_monitor", "lb_peek_cols", "lb_set_option"]
 
 
 class LBError(RuntimeError):
@@ -116,6 +116,7 @@ def lib():
         "lb_launch_count": (ctypes.c_int64, [vp]),
         "lb_set_peers": (i, [vp, p(lb_peers)]),
         "lb_monitor": (i, [vp, i]),
+        "lb_set_option": (i, [vp, i, i]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -389,6 +390,10 @@ class Lattice:
         P.right_buf[0], P.right_buf[1] = right_bufs
         P.left_done, P.right_done, P.my_done = left_done, right_done, my_done
         _check(lib().lb_set_peers(self._ctx, ctypes.byref(P)))
+
+    def set_propagate_impl(self, impl: str):
+        """'ldg' (default) or 'tma' (TMA-staged windows) for lb_propagate."""
+        _check(lib().lb_set_option(self._ctx, 0, {"ldg": 0, "tma": 1}[impl]))
 
     def monitor(self, enable: bool = True):
         """Fused monitors: invariants reduced inside the step kernel (lb_monitor)."""
