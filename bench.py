@@ -184,10 +184,13 @@ def kernel_passes(lb, lx_total, ly, fields, hbm_peak, fp64_peak, ncu, nsteps=10)
     """Per-kernel CUDA-event times of split BGK, fused regularised and split
     regularised steps on the same workload (library instrumentation)."""
     kern = {}
-    for mode, coll, impl in (("split", "bgk", "ldg"), ("split", "bgk", "tma"), ("fused", "regularized", "ldg"),
-                             ("split", "regularized", "ldg")):
+    for mode, coll, impl in (("split", "bgk", "ldg"), ("split", "bgk", "tma"), ("fused", "bgk", "tma"),
+                             ("fused", "regularized", "ldg"), ("split", "regularized", "ldg")):
         g = lb.Lattice(lx_total, ly, mode=mode, collision=coll)
-        g.set_propagate_impl(impl)
+        if mode == "split":
+            g.set_propagate_impl(impl)
+        else:
+            g.set_fused_impl(impl)
         g.init_macro(*fields)
         g.step(3)
         g.profile(True)
@@ -200,7 +203,8 @@ def kernel_passes(lb, lx_total, ly, fields, hbm_peak, fp64_peak, ncu, nsteps=10)
                 continue
             avg = v["total_ms"] / max(1, v["launches"])
             e = {"avg_ms": avg, "launches": v["launches"]}
-            if k in ("k_propagate", "k_propagate_tma", "k_collide", "k_collide_reg", "k_step_fused_reg"):
+            if k in ("k_propagate", "k_propagate_tma", "k_collide", "k_collide_reg", "k_step_fused_reg",
+                     "k_step_fused_tma"):
                 per = BYTES_PER_SITE * v["units"] / v["launches"]
                 e["gbs"] = per / (avg * 1e-3) / 1e9
                 e["hbm_frac"] = e["gbs"] / hbm_peak

@@ -286,7 +286,9 @@ int lb_sync(lb_ctx* ctx);
  * 16-byte vector stores; the default when the tensor maps can be encoded),
  * 0 = register gather with coalesced 8-byte loads, all 37 in flight per
  * thread.  Both are bit-identical; bench.py reports both. */
-enum lb_option { LB_OPT_PROPAGATE_IMPL = 0 };
+/* LB_OPT_FUSED_IMPL (lb_step, fused mode, N = 1 with walls, monitors off):
+ * 0 = register gather (default), 1 = TMA-staged windows in shared memory. */
+enum lb_option { LB_OPT_PROPAGATE_IMPL = 0, LB_OPT_FUSED_IMPL = 1 };
 int lb_set_option(lb_ctx* ctx, int option, int value);
 
 /* Fused monitors.  enable != 0: every fused step also reduces, per block, the

@@ -140,6 +140,7 @@ struct lb_ctx {
   unsigned long long peer_timeout_ns = 20000000000ull;
   lbk::TmaMaps* tma = nullptr;  // tensor maps of f_a / f_b (TMA propagate)
   int prop_impl = 0;            // LB_OPT_PROPAGATE_IMPL (1 = TMA when available)
+  int fused_impl = 0;           // LB_OPT_FUSED_IMPL (1 = TMA-staged windows)
   double omega = 1.0;
   lbd::Relax relax{};
   int64_t launches = 0;
@@ -364,7 +365,14 @@ int step_once(lb_ctx* c) {
     if (!c->halo_fresh) TRY(exchange_on(c, c->s));
     lbk::Halo h;
     h.dstL = h.dstR = c->B;
-    TRY(fused(c, all_cols(c), h));
+    if (c->fused_impl == 1 && c->tma && !c->mon_on) {
+      TRY(launch(c, c->p.collision ? "k_step_fused_reg_tma" : "k_step_fused_tma", c->s, c->L.sites, [&] {
+        return lbk::launch_step_fused_tma(c->g, c->tma, c->par, c->A, c->B, c->p.bc_y, c->p.collision, c->relax,
+                                          h, c->s);
+      }));
+    } else {
+      TRY(fused(c, all_cols(c), h));
+    }
     swap_ab(c);
     c->halo_fresh = true;
     fused_step_done(c);
@@ -795,6 +803,25 @@ int lb_set_peers(lb_ctx* c, const lb_peers* p) {
   for (int k = 0; k < 2; ++k)
     if (!p->left_buf[k] || !p->right_buf[k]) return fail(LB_EINVAL, "NULL peer buffer");
   if (!p->left_done || !p->right_done || !p->my_done) return fail(LB_EINVAL, "NULL step counter");
+  // memory of a neighbour on another GPU (CUDA-IPC mapping): make sure this
+  // device may access it directly (P2P over NVLink); same-device: nothing to do
+  int dev = 0;
+  CU(cudaGetDevice(&dev));
+  const void* ptrs[6] = {p->left_buf[0], p->left_buf[1], p->right_buf[0], p->right_buf[1], p->left_done,
+                         p->right_done};
+  for (const void* q : ptrs) {
+    cudaPointerAttributes a;
+    CU(cudaPointerGetAttributes(&a, q));
+    if (a.type != cudaMemoryTypeDevice) return fail(LB_EINVAL, "peer pointer is not device memory");
+    if (a.device != dev) {
+      int can = 0;
+      CU(cudaDeviceCanAccessPeer(&can, dev, a.device));
+      if (!can) return fail(LB_EINVAL, "device %d cannot access peer device %d", dev, a.device);
+      cudaError_t e = cudaDeviceEnablePeerAccess(a.device, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) (void)cudaGetLastError();
+      else if (e != cudaSuccess) return fail(LB_ECUDA, "peer access to device %d: %s", a.device, cudaGetErrorString(e));
+    }
+  }
   if (!c->d_status && cudaMalloc(&c->d_status, sizeof(unsigned int)) != cudaSuccess)
     return fail(LB_ENOMEM, "status allocation failed");
   CU(cudaMemsetAsync(c->d_status, 0, sizeof(unsigned int), c->s));
@@ -818,6 +845,11 @@ int lb_set_option(lb_ctx* c, int option, int value) {
         if (!c->tma) return fail(LB_ECUDA, "TMA tensor-map encoding unavailable");
       }
       c->prop_impl = value;
+      return LB_OK;
+    case LB_OPT_FUSED_IMPL:
+      if (value != 0 && value != 1) return fail(LB_EINVAL, "fused impl must be 0 (gather) or 1 (TMA)");
+      if (value == 1 && !c->tma) return fail(LB_ECUDA, "TMA tensor-map encoding unavailable");
+      c->fused_impl = value;
       return LB_OK;
     default:
       return fail(LB_EINVAL, "unknown option %d", option);

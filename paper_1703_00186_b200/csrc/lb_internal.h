@@ -1,5 +1,6 @@
 // lb_internal.h — host-side declarations shared by lb_kernels.cu and lb_api.cu.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstdint>
 
@@ -53,11 +54,17 @@ cudaError_t launch_step_fused(const Geo& g, const double* A, double* B, int bc, 
                               const lbd::Relax& r, Cols cols, const Halo& h, double* mon, cudaStream_t s);
 size_t monitor_slots(const Geo& g);
 cudaError_t launch_monitor_reduce(const double* mon, int64_t nslots, double* out, cudaStream_t s);
-// TMA-staged propagate (lb_tma.cu): tensor maps of both buffers, built once
-struct TmaMaps;
+// TMA-staged kernels (lb_tma.cu): tensor maps of both buffers, built once.
+// Buffer k viewed as {nyp rows, 37 populations, nx columns}, box {256, 1, 1}.
+struct TmaMaps {
+  CUtensorMap load[2];
+};
 TmaMaps* tma_create(const Geo& g, double* buf0, double* buf1);
 void tma_destroy(TmaMaps* t);
 cudaError_t launch_propagate_tma(const Geo& g, const TmaMaps* t, int src_buf, double* B, cudaStream_t s);
+// Fused step with TMA-staged windows (N = 1 local wrap path; walls only)
+cudaError_t launch_step_fused_tma(const Geo& g, const TmaMaps* t, int src_buf, const double* A, double* B,
+                                  int bc, int coll, const lbd::Relax& r, const Halo& h, cudaStream_t s);
 cudaError_t launch_signal(unsigned long long* done, unsigned long long v, cudaStream_t s);
 cudaError_t launch_peer_pull(const Geo& g, double* A, const double* left_A, const double* right_A,
                              cudaStream_t s);

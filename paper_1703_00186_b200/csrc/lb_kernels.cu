@@ -743,4 +743,102 @@ cudaError_t launch_monitor_reduce(const double* mon, int64_t nslots, double* out
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- fused step, TMA-staged
+// Same step as k_step_fused, but the 37 +-3-row windows of a 254-row tile are
+// brought into shared memory by TMA (one elected thread, one mbarrier; box
+// starts rounded down to 16 bytes, see lb_tma.cu) and each thread reads its
+// site's populations from smem.  Wall-band sites replace the populations whose
+// pull source lies beyond the wall with the specular image read from global
+// memory (the image rows can fall outside the loaded windows).
+constexpr int FT_TILE = 254;
+constexpr int FT_ROW = 256;
+constexpr int FT_THREADS = 256;
+constexpr size_t FT_SMEM = (size_t)Q * FT_ROW * sizeof(double) + 16;
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+template <int BC, int COLL>
+__global__ void __launch_bounds__(FT_THREADS, 2) k_step_fused_tma(const __grid_constant__ CUtensorMap src,
+                                                                  const double* __restrict__ A,
+                                                                  double* __restrict__ B, Geo g, Relax r,
+                                                                  Halo h) {
+  extern __shared__ __align__(1024) double sm[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + Q * FT_ROW);
+  const uint32_t b = smem_addr(bar);
+  const int ix = H + (int)blockIdx.y;
+  const int t = threadIdx.x;
+  const int y = (int)blockIdx.x * FT_TILE + t;  // physical row of this thread
+  const int r0 = g.y0 + (int)blockIdx.x * FT_TILE;
+  if (t == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (t == 0) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b),
+                 "r"((uint32_t)(Q * (FT_TILE + 2) * sizeof(double))));
+#pragma unroll
+    for (int l = 0; l < Q; ++l) {
+      const int base = r0 - CY(l) - (CY(l) & 1);
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+          " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_addr(sm + l * FT_ROW)),
+          "l"(&src), "r"(base), "r"(l), "r"(ix - CX(l)), "r"(b)
+          : "memory");
+    }
+  }
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+      " @!p bra WAIT_%=;\n"
+      "}\n" ::"r"(b)
+      : "memory");
+  if (t >= FT_TILE || y >= g.ly) return;
+  double f[Q];
+#pragma unroll
+  for (int l = 0; l < Q; ++l) f[l] = sm[l * FT_ROW + t + (CY(l) & 1)];
+  if (y < 3 || y >= g.ly - 3) {
+    const int64_t colbase = (int64_t)g.y0;
+#pragma unroll
+    for (int l = 0; l < Q; ++l) {
+      const int sy = y - CY(l);
+      int ys = -1;
+      if (sy < 0) ys = -1 - sy;
+      else if (sy >= g.ly) ys = 2 * g.ly - 1 - sy;
+      if (ys >= 0) f[l] = __ldg(A + (int64_t)(ix - CX(l)) * g.cs + (int64_t)refl(l) * g.nyp + colbase + ys);
+    }
+    if (BC == BC_THERMAL) thermal_wall(f, y < 3 ? 0 : 1);
+  }
+  collide_any<COLL>(f, r);
+  store_site(B, g, ix, y, f);
+  if (h.dstL != nullptr && ix < 2 * H) store_site(h.dstL, g, ix + g.lx, y, f);
+  if (h.dstR != nullptr && ix >= g.lx) store_site(h.dstR, g, ix - g.lx, y, f);
+}
+
+template <int BC, int COLL>
+cudaError_t launch_ft(const Geo& g, const TmaMaps* t, int src_buf, const double* A, double* B, const Relax& r,
+                      const Halo& h, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_step_fused_tma<BC, COLL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)FT_SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  dim3 grid((g.ly + FT_TILE - 1) / FT_TILE, g.lx);
+  k_step_fused_tma<BC, COLL><<<grid, FT_THREADS, FT_SMEM, s>>>(t->load[src_buf], A, B, g, r, h);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_step_fused_tma(const Geo& g, const TmaMaps* t, int src_buf, const double* A, double* B,
+                                  int bc, int coll, const Relax& r, const Halo& h, cudaStream_t s) {
+  if (bc == BC_THERMAL)
+    return coll == COLL_REGULARIZED ? launch_ft<BC_THERMAL, COLL_REGULARIZED>(g, t, src_buf, A, B, r, h, s)
+                                    : launch_ft<BC_THERMAL, COLL_BGK>(g, t, src_buf, A, B, r, h, s);
+  return coll == COLL_REGULARIZED ? launch_ft<BC_ADIABATIC, COLL_REGULARIZED>(g, t, src_buf, A, B, r, h, s)
+                                  : launch_ft<BC_ADIABATIC, COLL_BGK>(g, t, src_buf, A, B, r, h, s);
+}
+
 }  // namespace lbk

@@ -29,10 +29,6 @@ constexpr int TMA_ROW = 256;               // smem row pitch: 128-byte aligned b
 constexpr int TMA_THREADS = 128;
 constexpr size_t TMA_SMEM = (size_t)Q * TMA_ROW * sizeof(double) + 16;
 
-struct TmaMaps {
-  CUtensorMap load[2];  // buffer 0 / 1 viewed as {nyp rows, 37 populations, nx columns}
-};
-
 namespace {
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

@@ -395,6 +395,10 @@ class Lattice:
         """'ldg' (default) or 'tma' (TMA-staged windows) for lb_propagate."""
         _check(lib().lb_set_option(self._ctx, 0, {"ldg": 0, "tma": 1}[impl]))
 
+    def set_fused_impl(self, impl: str):
+        """'ldg' (default) or 'tma' for the fused step kernel (N=1, walls)."""
+        _check(lib().lb_set_option(self._ctx, 1, {"ldg": 0, "tma": 1}[impl]))
+
     def monitor(self, enable: bool = True):
         """Fused monitors: invariants reduced inside the step kernel (lb_monitor)."""
         _check(lib().lb_monitor(self._ctx, int(enable)))

@@ -474,3 +474,21 @@ def test_tma_propagate_bit_exact(lb, bc, shape):
         g.bc(); ref.bc()
         g.collide(); ref.collide()
     assert np.array_equal(g.gather(), ref.gather())
+
+
+@pytest.mark.parametrize("coll", ["bgk", "regularized"])
+@pytest.mark.parametrize("bc", ["thermal", "adiabatic"])
+@pytest.mark.parametrize("shape", [(24, 6), (17, 131), (9, 300), (40, 509)])
+def test_tma_fused_step_bit_identical(lb, coll, bc, shape):
+    """LB_OPT_FUSED_IMPL = 1 (TMA-staged windows) == the register-gather fused
+    step bit for bit (multi-tile columns, ragged last tile, wall bands)."""
+    lx, ly = shape
+    st = oracle_state(lx, ly, seed=lx + ly)
+    outs = []
+    for impl in ("ldg", "tma"):
+        g = lb.Lattice(lx, ly, bc_y=bc, collision=coll, gravity=(0.0, -1e-5))
+        g.set_fused_impl(impl)
+        g.set_state(st)
+        g.step(5)
+        outs.append(g.gather())
+    assert np.array_equal(outs[0], outs[1])
