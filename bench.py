@@ -305,11 +305,13 @@ def main():
     barrier()
     stream = torch.cuda.current_stream()
 
-    # ---- warm-up, then exactly K timed steps (device time, max over ranks)
+    # ---- warm-up, then exactly K timed steps (device time, max over ranks).
+    # The headline region carries no per-launch events (they cost ~1 % of a
+    # step); the dominant kernel's launch durations are measured live in a
+    # second timed region of K steps right after it, with the library's
+    # per-launch CUDA events on the launch stream.
     g.step(args.warmup)
     g.sync()
-    g.profile(True)
-    g.profile_reset()
     launches0 = g.launch_count()
     barrier()
     torch.cuda.synchronize()
@@ -323,8 +325,17 @@ def main():
     barrier()
     launches = g.launch_count() - launches0
     ms = max_over_ranks(e0.elapsed_time(e1))
+    g.profile(True)
+    g.profile_reset()
+    barrier()
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    g.step(args.steps)
+    e3.record(stream)
+    g.sync()
     prof = g.profile_read()
     g.profile(False)
+    ms_prof = e2.elapsed_time(e3)
     sites_all = lx_total * ly
     value = pm.mlups(sites_all * args.steps, ms * 1e-3)   # Table 1 convention (tests/test_metrics.py)
 
@@ -357,7 +368,9 @@ def main():
                     "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
                     "traffic": (traffic * fk["units"] / fk["launches"]) if traffic else None,
                     "algorithmic_bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_ms,
-                    "share_of_step": fk["total_ms"] / ms if world == 1 else None,
+                    "share_of_step": fk["total_ms"] / ms_prof,
+                    "measured": "per-launch CUDA events on the launch stream over a second timed region "
+                                f"of the same {args.steps} steps",
                     "peak_source": peak_src,
                     "traffic_source": ncu.get("source") if traffic else None}
 

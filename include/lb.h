@@ -288,7 +288,11 @@ int lb_sync(lb_ctx* ctx);
  * thread.  Both are bit-identical; bench.py reports both. */
 /* LB_OPT_FUSED_IMPL (lb_step, fused mode, N = 1 with walls, monitors off):
  * 0 = register gather (default), 1 = TMA-staged windows in shared memory. */
-enum lb_option { LB_OPT_PROPAGATE_IMPL = 0, LB_OPT_FUSED_IMPL = 1 };
+/* LB_OPT_CUDA_GRAPH (value 1): lb_step replays CUDA graphs of two steps in the
+ * steady state of the fused N = 1 path and of the peer path (bit-identical;
+ * fewer host launches, matters for small lattices).  Needs a non-default
+ * context stream; ignored while profiling. */
+enum lb_option { LB_OPT_PROPAGATE_IMPL = 0, LB_OPT_FUSED_IMPL = 1, LB_OPT_CUDA_GRAPH = 2 };
 int lb_set_option(lb_ctx* ctx, int option, int value);
 
 /* Fused monitors.  enable != 0: every fused step also reduces, per block, the

@@ -141,6 +141,10 @@ struct lb_ctx {
   lbk::TmaMaps* tma = nullptr;  // tensor maps of f_a / f_b (TMA propagate)
   int prop_impl = 0;            // LB_OPT_PROPAGATE_IMPL (1 = TMA when available)
   int fused_impl = 0;           // LB_OPT_FUSED_IMPL (1 = TMA-staged windows)
+  bool graph_on = false;        // LB_OPT_CUDA_GRAPH: lb_step replays 2-step graphs
+  cudaGraphExec_t gexec[2] = {nullptr, nullptr};  // keyed by the parity at graph start
+  int gkey[2] = {-1, -1};       // configuration each graph was captured for
+  int64_t glaunch[2] = {0, 0};  // kernel launches inside each graph
   double omega = 1.0;
   lbd::Relax relax{};
   int64_t launches = 0;
@@ -152,6 +156,10 @@ struct lb_ctx {
   std::vector<double> kms;
   std::vector<int64_t> kcount, kunits;
 };
+
+extern "C" {
+static void graph_reset(lb_ctx* c);
+}
 
 namespace {
 
@@ -336,13 +344,13 @@ int step_peer(lb_ctx* c) {
   h.dstR = P.right_buf[c->par ^ 1];
   h.waitL = reinterpret_cast<const unsigned long long*>(P.left_done);
   h.waitR = reinterpret_cast<const unsigned long long*>(P.right_done);
-  h.wait_val = c->peer_step;
+  h.my_done = reinterpret_cast<const unsigned long long*>(P.my_done);
   h.status = c->d_status;
   h.timeout_ns = c->peer_timeout_ns;
   TRY(fused(c, all_cols(c), h));
   c->peer_step += 1;
   TRY(launch(c, "k_signal", c->s, 0, [&] {
-    return lbk::launch_signal(reinterpret_cast<unsigned long long*>(P.my_done), c->peer_step, c->s);
+    return lbk::launch_signal(reinterpret_cast<unsigned long long*>(P.my_done), c->s);
   }));
   swap_ab(c);
   c->halo_fresh = true;
@@ -573,6 +581,7 @@ void lb_destroy(lb_ctx* c) {
   if (c->d_mon) cudaFree(c->d_mon);
   if (c->d_status) cudaFree(c->d_status);
   if (c->tma) lbk::tma_destroy(c->tma);
+  graph_reset(c);
   if (c->h_pin) cudaFreeHost(c->h_pin);
   delete c;
 }
@@ -686,10 +695,71 @@ int lb_collide(lb_ctx* c) {
   return LB_OK;
 }
 
+// CUDA-graph stepping (LB_OPT_CUDA_GRAPH): in the steady state of the fused
+// N = 1 wrap path and of the peer path every step issues the same launches
+// with the same parameters (the peer wait target is read on the device), and
+// two steps return A/B to their places — so two steps are captured once per
+// starting parity and replayed with one cudaGraphLaunch.
+static int graph_config(const lb_ctx* c) {
+  return c->fused_impl | (c->mon_on ? 2 : 0) | (c->peers_on ? 4 : 0);
+}
+
+static bool graphable(const lb_ctx* c) {
+  return c->graph_on && !c->prof && c->s != nullptr && c->p.mode == LB_MODE_FUSED && c->halo_fresh &&
+         (c->peers_on || (c->nranks == 1 && !c->comm && c->p.bc_y != LB_PERIODIC));
+}
+
+static void graph_reset(lb_ctx* c) {
+  for (int k = 0; k < 2; ++k) {
+    if (c->gexec[k]) cudaGraphExecDestroy(c->gexec[k]);
+    c->gexec[k] = nullptr;
+    c->gkey[k] = -1;
+  }
+}
+
+static int graph_two_steps(lb_ctx* c) {
+  const int par = c->par, key = graph_config(c);
+  if (!c->gexec[par] || c->gkey[par] != key) {
+    if (c->gexec[par]) cudaGraphExecDestroy(c->gexec[par]);
+    c->gexec[par] = nullptr;
+    const int64_t l0 = c->launches;
+    CU(cudaStreamBeginCapture(c->s, cudaStreamCaptureModeThreadLocal));
+    int r = step_once(c);
+    if (r == LB_OK) r = step_once(c);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(c->s, &graph);
+    c->glaunch[par] = c->launches - l0;
+    c->launches = l0;  // captured, not executed
+    if (r != LB_OK) return r;
+    if (e != cudaSuccess) return fail(LB_ECUDA, "graph capture failed: %s", cudaGetErrorString(e));
+    const cudaError_t ei = cudaGraphInstantiate(&c->gexec[par], graph, 0);
+    cudaGraphDestroy(graph);
+    if (ei != cudaSuccess) return fail(LB_ECUDA, "graph instantiation failed: %s", cudaGetErrorString(ei));
+    c->gkey[par] = key;
+  } else {
+    // host-side effects of two steps (the capture above performed them)
+    swap_ab(c);
+    swap_ab(c);
+    fused_step_done(c);
+  }
+  CU(cudaGraphLaunch(c->gexec[par], c->s));
+  c->launches += c->glaunch[par];
+  return LB_OK;
+}
+
 int lb_step(lb_ctx* c, int nsteps) {
   TRY(check_boundary(c, "lb_step"));
   if (nsteps < 0) return fail(LB_EINVAL, "nsteps < 0");
-  for (int k = 0; k < nsteps; ++k) TRY(step_once(c));
+  int k = 0;
+  while (k < nsteps) {
+    if (nsteps - k >= 2 && graphable(c)) {
+      TRY(graph_two_steps(c));
+      k += 2;
+    } else {
+      TRY(step_once(c));
+      k += 1;
+    }
+  }
   return LB_OK;
 }
 
@@ -845,6 +915,11 @@ int lb_set_option(lb_ctx* c, int option, int value) {
         if (!c->tma) return fail(LB_ECUDA, "TMA tensor-map encoding unavailable");
       }
       c->prop_impl = value;
+      return LB_OK;
+    case LB_OPT_CUDA_GRAPH:
+      if (value && !c->s) return fail(LB_EINVAL, "CUDA graphs need a non-default context stream");
+      c->graph_on = value != 0;
+      if (!c->graph_on) graph_reset(c);
       return LB_OK;
     case LB_OPT_FUSED_IMPL:
       if (value != 0 && value != 1) return fail(LB_EINVAL, "fused impl must be 0 (gather) or 1 (TMA)");

@@ -45,7 +45,10 @@ struct Halo {
   double* dstR = nullptr;   // ix in [lx, lx+3) -> column ix - lx of dstR
   const unsigned long long* waitL = nullptr;
   const unsigned long long* waitR = nullptr;
-  unsigned long long wait_val = 0;
+  // this rank's own counter = steps it has completed; the border blocks wait
+  // until both neighbours' counters reach it (read on device: the launch
+  // parameters are the same every step, so steps can be replayed from a graph)
+  const unsigned long long* my_done = nullptr;
   unsigned int* status = nullptr;      // set to 1 if a wait timed out (watchdog)
   unsigned long long timeout_ns = 0;   // 0: wait forever
 };
@@ -65,7 +68,8 @@ cudaError_t launch_propagate_tma(const Geo& g, const TmaMaps* t, int src_buf, do
 // Fused step with TMA-staged windows (N = 1 local wrap path; walls only)
 cudaError_t launch_step_fused_tma(const Geo& g, const TmaMaps* t, int src_buf, const double* A, double* B,
                                   int bc, int coll, const lbd::Relax& r, const Halo& h, cudaStream_t s);
-cudaError_t launch_signal(unsigned long long* done, unsigned long long v, cudaStream_t s);
+// this rank's counter += 1 (system-scope release), after the step kernel
+cudaError_t launch_signal(unsigned long long* done, cudaStream_t s);
 cudaError_t launch_peer_pull(const Geo& g, double* A, const double* left_A, const double* right_A,
                              cudaStream_t s);
 cudaError_t launch_init_macro(const Geo& g, double* A, const double* rho, const double* ux,

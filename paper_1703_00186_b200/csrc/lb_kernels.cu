@@ -393,7 +393,7 @@ cudaError_t launch_collide(const Geo& g, double* B, const Relax& r, int coll, cu
 // dstL = dstR = own B.  Peer mode (N > 1, include/lb.h lb_set_peers): dstL /
 // dstR are the neighbours' buffers mapped into this process (NVLink P2P
 // stores), and before touching any halo the border blocks wait until both
-// neighbours have completed the previous step (h.waitL/R >= h.wait_val): that
+// neighbours have completed the previous step (h.waitL/R >= *h.my_done): that
 // both makes this rank's halo current and the neighbour's halo free to
 // overwrite.  Bulk blocks never wait, so the exchange overlaps the bulk inside
 // one grid (P:585-613 without a communication stream).
@@ -489,7 +489,8 @@ __global__ void __launch_bounds__(TPB, BC == BC_PERIODIC ? 3 : 4) k_step_fused(c
       // GPU — after timeout_ns the block flags *status and proceeds (the step
       // result is then invalid; the host reports LB_EPEER at the next sync)
       const unsigned long long t0 = globaltimer_ns();
-      while (ld_acquire_sys(h.waitL) < h.wait_val || ld_acquire_sys(h.waitR) < h.wait_val) {
+      const unsigned long long want = *h.my_done;  // steps this rank has completed
+      while (ld_acquire_sys(h.waitL) < want || ld_acquire_sys(h.waitR) < want) {
         __nanosleep(128);
         if (h.timeout_ns && globaltimer_ns() - t0 > h.timeout_ns) {
           atomicExch(h.status, 1u);
@@ -571,15 +572,17 @@ cudaError_t launch_step_fused(const Geo& g, const double* A, double* B, int bc, 
 
 cudaError_t launch_monitor_reduce(const double* mon, int64_t nslots, double* out, cudaStream_t s);
 
-// Step signal of peer mode: this rank's counter := v (system-scope release),
-// after the fused kernel (stream order) and its border blocks' system fences.
-__global__ void k_signal(unsigned long long* done, unsigned long long v) {
+// Step signal of peer mode: this rank's counter += 1 (only this rank writes
+// it; system-scope release), after the fused kernel (stream order) and its
+// border blocks' system fences.
+__global__ void k_signal(unsigned long long* done) {
   __threadfence_system();
+  const unsigned long long v = *done + 1;
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(done), "l"(v) : "memory");
 }
 
-cudaError_t launch_signal(unsigned long long* done, unsigned long long v, cudaStream_t s) {
-  k_signal<<<1, 1, 0, s>>>(done, v);
+cudaError_t launch_signal(unsigned long long* done, cudaStream_t s) {
+  k_signal<<<1, 1, 0, s>>>(done);
   return cudaGetLastError();
 }
 

@@ -399,6 +399,10 @@ class Lattice:
         """'ldg' (default) or 'tma' for the fused step kernel (N=1, walls)."""
         _check(lib().lb_set_option(self._ctx, 1, {"ldg": 0, "tma": 1}[impl]))
 
+    def use_graphs(self, enable: bool = True):
+        """Replay 2-step CUDA graphs in lb_step (needs a non-default stream)."""
+        _check(lib().lb_set_option(self._ctx, 2, int(enable)))
+
     def monitor(self, enable: bool = True):
         """Fused monitors: invariants reduced inside the step kernel (lb_monitor)."""
         _check(lib().lb_monitor(self._ctx, int(enable)))
