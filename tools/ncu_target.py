@@ -1,6 +1,7 @@
-"""Small target for ncu: a few steps per (mode, collision) at 1920x2048.
+"""Small target for ncu: a few steps per spec at 1920x2048.
 
-ncu ... python tools/ncu_target.py fused split fused:regularized split:regularized
+spec = mode[:collision[:impl]]   e.g.  fused  split  fused:regularized  split:bgk:ldg  fused:bgk:tma
+ncu ... python tools/ncu_target.py fused split fused:regularized split:regularized split:bgk:ldg
 """
 import os
 import sys
@@ -14,8 +15,13 @@ import paper_1703_00186_b200 as lb  # noqa: E402
 lx, ly = int(os.environ.get("LB_LX", 1920)), int(os.environ.get("LB_LY", 2048))
 fields = lbgen.rt_macro(lx, ly, lb.t0())
 for spec in sys.argv[1:] or ["fused", "split"]:
-    mode, _, coll = spec.partition(":")
-    g = lb.Lattice(lx, ly, mode=mode, collision=coll or "bgk")
+    parts = spec.split(":")
+    mode = parts[0]
+    coll = parts[1] if len(parts) > 1 else "bgk"
+    impl = parts[2] if len(parts) > 2 else None
+    g = lb.Lattice(lx, ly, mode=mode, collision=coll)
+    if impl:
+        (g.set_propagate_impl if mode == "split" else g.set_fused_impl)(impl)
     g.init_macro(*fields)
     g.step(3)
     g.sync()
