@@ -221,6 +221,28 @@ def test_call_order_errors(lb):
     g.gather()
 
 
+def test_api_error_paths(lb):
+    """Documented LB_EINVAL / LB_ESTATE cases of include/lb.h."""
+    def status(fn):
+        with pytest.raises(lb.LBError) as ei:
+            fn()
+        return ei.value.status
+    g = lb.Lattice(16, 16)                      # default (legacy) stream
+    assert status(lambda: g.use_graphs(True)) == 1
+    assert status(lambda: lb.lib().lb_set_option(g._ctx, 99, 1) and lb.lb._check(
+        lb.lib().lb_set_option(g._ctx, 99, 1))) == 1
+    s = lb.Lattice(16, 16, mode="split")
+    assert status(lambda: s.set_peers(s, s)) == 1        # peers need fused mode
+    p = lb.Lattice(16, 16, bc_y="periodic")
+    assert status(lambda: p.set_peers(p, p)) == 1        # and walls
+    a, b = (lb.Lattice(32, 16, rank=r, nranks=2) for r in range(2))
+    assert status(lambda: a.step(1)) == 2                # N > 1 without NCCL or peers
+    assert status(lambda: a.gather()) == 2               # gather needs the communicator
+    assert status(lambda: a.peek_cols(10, 10)) == 1      # column range out of bounds
+    for x in (g, s, p, a, b):
+        x.close()
+
+
 # ------------------------------------------------------------------ full size (config #2)
 
 @pytest.mark.parametrize("overlap", [False, True])
@@ -538,3 +560,37 @@ def test_graph_steps_peer_ring(lb):
         g.sync()
     got = np.concatenate([g.peek(0) for g in ranks], axis=1)
     assert np.array_equal(got, ref.gather())
+
+
+@pytest.mark.parametrize("lx_total,ly,n", [(64, 32, 2), (48, 64, 4), (96, 32, 8), (48, 64, 8)])
+def test_peer_ring_survey_geometries_with_injected_delay(lb, lx_total, ly, n):
+    """SURVEY §4 multi-GPU tier geometries (64x32, 48x64, 96x32 at N = 2..8) as
+    in-process peer rings, with an injected delay (a sleep kernel) in front of
+    every step of one rank (SPEC S:292 'injected-delay regime'): the step
+    counters must order everything, the result is the 1-slab run bit for bit."""
+    nsteps = 6
+    T0 = oracle.t0()
+    ref = lb.Lattice(lx_total, ly)
+    ref.init_macro(*lbgen.rt_macro(lx_total, ly, T0))
+    ref.step(nsteps)
+    lx = lx_total // n
+    streams = [torch.cuda.Stream() for _ in range(n)]
+    ranks = [lb.Lattice(lx_total, ly, rank=r, nranks=n, stream=streams[r]) for r in range(n)]
+    for r, g in enumerate(ranks):
+        g.init_macro(*lbgen.rt_macro(lx_total, ly, T0, x0=r * lx, lx=lx))
+    for r, g in enumerate(ranks):
+        g.set_peers(ranks[(r - 1) % n], ranks[(r + 1) % n])
+    torch.cuda.synchronize()
+    slow = n // 2
+    for _ in range(nsteps):
+        for r, g in enumerate(ranks):
+            if r == slow:
+                with torch.cuda.stream(streams[r]):
+                    torch.cuda._sleep(2_000_000)   # ~1 ms of spinning before this rank's step
+            g.step(1)
+    for g in ranks:
+        g.sync()
+    got = np.concatenate([g.peek(0) for g in ranks], axis=1)
+    assert np.array_equal(got, ref.gather())
+    for g in ranks:
+        g.close()
