@@ -1,6 +1,6 @@
 """BASELINE config #5 on one GPU: D2Q37 fp64 2048x4096 Rayleigh-Taylor long run.
 
-    python tools/long_run.py [--steps 10000] [--every 100] [--ckpt-every 1000]
+    python tests/long_run.py [--steps 10000] [--every 100] [--ckpt-every 1000]
                              [--check 10] [--gravity 0] [--out profiles/r01_long_run.json]
 
 The fused GPU path runs `steps` steps; lb_invariants every `every` steps

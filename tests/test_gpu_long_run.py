@@ -1,4 +1,4 @@
-"""Config #5 machinery (tools/long_run.py) at a reduced size: invariants series,
+"""Config #5 machinery (tests/long_run.py) at a reduced size: invariants series,
 LBFIELD checkpoints and oracle checkpoint-restart parity <= 1e-12."""
 import os
 import sys
@@ -7,7 +7,7 @@ import pytest
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
-sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 
 
 @pytest.mark.parametrize("gravity", [0.0, 1e-4])
