@@ -232,6 +232,7 @@ int validate(const lb_params* p, int rank, int nranks) {
   if (p->lx_total <= 0 || p->lx_total % nranks) return fail(LB_EINVAL, "lx_total %% nranks != 0");
   const int lx = p->lx_total / nranks;
   if (lx < (nranks == 1 ? 3 : 6)) return fail(LB_EINVAL, "per-rank lx = %d too small", lx);
+  if (lx > 65535) return fail(LB_EINVAL, "per-rank lx = %d exceeds the 65535-column grid limit", lx);
   if (p->bc_y < 0 || p->bc_y > 2) return fail(LB_EINVAL, "bad bc_y");
   if (p->ly < (p->bc_y == LB_PERIODIC ? 3 : 6)) return fail(LB_EINVAL, "ly = %d too small", p->ly);
   if (p->mode < 0 || p->mode > 1) return fail(LB_EINVAL, "bad mode");

@@ -823,12 +823,15 @@ __global__ void __launch_bounds__(FT_THREADS, 2) k_step_fused_tma(const __grid_c
 template <int BC, int COLL>
 cudaError_t launch_ft(const Geo& g, const TmaMaps* t, int src_buf, const double* A, double* B, const Relax& r,
                       const Halo& h, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_step_fused_tma<BC, COLL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)FT_SMEM);
+  // opt-in shared memory is a per-device function attribute: set it once per device
+  static unsigned long long done_mask = 0;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev >= 64 || !(done_mask >> dev & 1ull)) {
+    e = cudaFuncSetAttribute(k_step_fused_tma<BC, COLL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FT_SMEM);
     if (e != cudaSuccess) return e;
-    attr = true;
+    if (dev < 64) done_mask |= 1ull << dev;
   }
   dim3 grid((g.ly + FT_TILE - 1) / FT_TILE, g.lx);
   k_step_fused_tma<BC, COLL><<<grid, FT_THREADS, FT_SMEM, s>>>(t->load[src_buf], A, B, g, r, h);

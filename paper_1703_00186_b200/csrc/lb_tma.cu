@@ -127,11 +127,15 @@ TmaMaps* tma_create(const Geo& g, double* buf0, double* buf1) {
 void tma_destroy(TmaMaps* t) { delete t; }
 
 cudaError_t launch_propagate_tma(const Geo& g, const TmaMaps* t, int src_buf, double* B, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_propagate_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TMA_SMEM);
+  // opt-in shared memory is a per-device function attribute: set it once per device
+  static unsigned long long done_mask = 0;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev >= 64 || !(done_mask >> dev & 1ull)) {
+    e = cudaFuncSetAttribute(k_propagate_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TMA_SMEM);
     if (e != cudaSuccess) return e;
-    attr = true;
+    if (dev < 64) done_mask |= 1ull << dev;
   }
   dim3 grid((g.ly + TMA_TILE - 1) / TMA_TILE, g.lx);
   k_propagate_tma<<<grid, TMA_THREADS, TMA_SMEM, s>>>(t->load[src_buf], B, g);
