@@ -279,6 +279,11 @@ int lb_peek_cols(lb_ctx* ctx, int which, int x0, int ncols, double* host_out);
  * LB_ENONPHYS if any value is NaN or min rho <= 0.  Synchronising. */
 int lb_invariants(lb_ctx* ctx, double* out);
 
+/* Non-blocking variant: enqueues the same reduction (collective) and an async
+ * copy of the 5 values into host_out (page-locked memory for true asynchrony),
+ * valid after the next lb_sync; no NaN / rho checks are made. */
+int lb_invariants_async(lb_ctx* ctx, double* host_out);
+
 int lb_sync(lb_ctx* ctx);
 
 /* Options.  LB_OPT_PROPAGATE_IMPL (lb_propagate, split mode): 1 = TMA-staged

@@ -836,9 +836,9 @@ int lb_peek(lb_ctx* c, int which, double* host_out) {
   return lb_peek_cols(c, which, 0, c->g.lx, host_out);
 }
 
-int lb_invariants(lb_ctx* c, double* out) {
-  TRY(check_boundary(c, "lb_invariants"));
-  if (!out) return fail(LB_EINVAL, "out is NULL");
+// Enqueue the invariants of A (fused-monitor partials when valid, else a full
+// pass), the cross-rank reduction, and their D2H copy to host_dst.
+static int invariants_enqueue(lb_ctx* c, double* host_dst) {
   double* res = c->d_part + lbk::invariants_scratch(c->g);
   if (c->mon_valid) {
     TRY(launch(c, "k_monitor_reduce", c->s, 0, [&] {
@@ -855,7 +855,14 @@ int lb_invariants(lb_ctx* c, double* out) {
     NC(ncclAllReduce(res + 4, res + 4, 1, ncclDouble, ncclMin, c->comm, c->s));
     NC(ncclGroupEnd());
   }
-  CU(cudaMemcpyAsync(c->h_pin, res, 5 * sizeof(double), cudaMemcpyDeviceToHost, c->s));
+  CU(cudaMemcpyAsync(host_dst, res, 5 * sizeof(double), cudaMemcpyDeviceToHost, c->s));
+  return LB_OK;
+}
+
+int lb_invariants(lb_ctx* c, double* out) {
+  TRY(check_boundary(c, "lb_invariants"));
+  if (!out) return fail(LB_EINVAL, "out is NULL");
+  TRY(invariants_enqueue(c, c->h_pin));
   CU(cudaStreamSynchronize(c->s));
   TRY(check_peer_status(c));
   std::memcpy(out, c->h_pin, 5 * sizeof(double));
@@ -863,6 +870,12 @@ int lb_invariants(lb_ctx* c, double* out) {
     if (std::isnan(out[k])) return fail(LB_ENONPHYS, "NaN in invariants");
   if (!(out[4] > 0.0)) return fail(LB_ENONPHYS, "site density <= 0 or NaN");
   return LB_OK;
+}
+
+int lb_invariants_async(lb_ctx* c, double* host_out) {
+  TRY(check_boundary(c, "lb_invariants_async"));
+  if (!host_out) return fail(LB_EINVAL, "host_out is NULL");
+  return invariants_enqueue(c, host_out);
 }
 
 int lb_set_peers(lb_ctx* c, const lb_peers* p) {

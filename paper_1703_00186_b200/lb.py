@@ -30,7 +30,7 @@ EXPORTS = ["lb_query_layout", "lb_exchange_plan", "lb_constants", "lb_kwall", "l
            "lb_set_state", "lb_exchange", "lb_propagate", "lb_bc", "lb_collide", "lb_step",
            "lb_gather", "lb_peek", "lb_invariants", "lb_sync", "lb_profile_enable",
            "lb_profile_reset", "lb_profile_read", "lb_launch_count", "lb_set_peers",
-           "lb_monitor", "lb_peek_cols", "lb_set_option"]
+           "lb_monitor", "lb_peek_cols", "lb_set_option", "lb_invariants_async"]
 
 
 class LBError(RuntimeError):
@@ -110,6 +110,7 @@ def lib():
         "lb_peek": (i, [vp, i, vp]),
         "lb_peek_cols": (i, [vp, i, i, i, vp]),
         "lb_invariants": (i, [vp, vp]),
+        "lb_invariants_async": (i, [vp, vp]),
         "lb_sync": (i, [vp]),
         "lb_profile_enable": (i, [vp, i]), "lb_profile_reset": (i, [vp]),
         "lb_profile_read": (i, [vp, p(lb_kprof), i, p(i)]),
@@ -310,6 +311,17 @@ class Lattice:
         out = np.empty((Q, self.lx, self.ly))
         _check(lib().lb_peek(self._ctx, which, _dptr(out)))
         return out
+
+    def invariants_async(self, out) -> None:
+        """Enqueue the invariants into `out` (5 float64, ideally a pinned torch
+        tensor / its numpy view); valid after sync()."""
+        import torch
+        if isinstance(out, torch.Tensor):
+            assert out.dtype == torch.float64 and out.numel() >= 5 and not out.is_cuda
+            ptr = ctypes.c_void_p(out.data_ptr())
+        else:
+            ptr = _dptr(out)
+        _check(lib().lb_invariants_async(self._ctx, ptr))
 
     def peek_cols(self, x0: int, ncols: int, which: int = 0) -> np.ndarray:
         """Local physical columns [x0, x0+ncols) of A (0) or B (1): [37][ncols][ly]."""
