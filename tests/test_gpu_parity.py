@@ -438,6 +438,26 @@ def test_gravity_free_fall_periodic(lb):
 
 # ------------------------------------------------------------------ fused monitors
 
+def test_invariants_async_matches_sync(lb):
+    lx, ly = 40, 64
+    g = lb.Lattice(lx, ly)
+    g.init_macro(*lbgen.rt_macro(lx, ly, oracle.t0()))
+    g.monitor(True)
+    out = torch.zeros((6, 5), dtype=torch.float64).pin_memory()
+    sync_vals = []
+    for k in range(3):
+        g.step(1)
+        g.invariants_async(out[k])
+    g.sync()
+    ref = lb.Lattice(lx, ly)
+    ref.init_macro(*lbgen.rt_macro(lx, ly, oracle.t0()))
+    ref.monitor(True)
+    for k in range(3):
+        ref.step(1)
+        sync_vals.append(ref.invariants())
+    assert np.array_equal(out[:3].numpy(), np.array(sync_vals))
+
+
 @pytest.mark.parametrize("overlap,nccl", [(False, False), (True, True)])
 def test_fused_monitors(lb, overlap, nccl):
     """Monitored fused steps leave the state bit-identical, and the in-kernel
