@@ -348,7 +348,9 @@ int step_peer(lb_ctx* c) {
   h.my_done = reinterpret_cast<const unsigned long long*>(P.my_done);
   h.status = c->d_status;
   h.timeout_ns = c->peer_timeout_ns;
-  TRY(fused(c, all_cols(c), h));
+  Cols cc = all_cols(c);
+  cc.rev = c->par;  // alternate the column order: start on what the last step wrote (L2)
+  TRY(fused(c, cc, h));
   c->peer_step += 1;
   TRY(launch(c, "k_signal", c->s, 0, [&] {
     return lbk::launch_signal(reinterpret_cast<unsigned long long*>(P.my_done), c->s);
@@ -380,7 +382,9 @@ int step_once(lb_ctx* c) {
                                           h, c->s);
       }));
     } else {
-      TRY(fused(c, all_cols(c), h));
+      Cols cc = all_cols(c);
+      cc.rev = c->par;  // alternate the column order: start on what the last step wrote (L2)
+      TRY(fused(c, cc, h));
     }
     swap_ab(c);
     c->halo_fresh = true;

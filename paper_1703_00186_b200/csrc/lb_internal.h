@@ -22,8 +22,12 @@ enum CollKind { COLL_BGK = 0, COLL_REGULARIZED = 1 };
 
 // Column ranges are in internal column indices (physical columns are
 // [3, 3+lx)).  A launch covers [xa0, xa1) U [xb0, xb1).
+// rev != 0: blocks take the columns in reverse order (alternated step by step,
+// so a step starts on the columns the previous step wrote last: those are
+// still in the 126 MB L2 and are read from there instead of HBM).
 struct Cols {
   int xa0, xa1, xb0, xb1;
+  int rev = 0;
   int count() const { return (xa1 - xa0) + (xb1 - xb0); }
 };
 

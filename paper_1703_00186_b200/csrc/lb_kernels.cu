@@ -480,7 +480,8 @@ __global__ void __launch_bounds__(TPB, BC == BC_PERIODIC ? 3 : 4) k_step_fused(c
                                                     Relax r, Halo h, double* __restrict__ mon) {
   const int y = blockIdx.x * TPB + threadIdx.x;
   const int na = cols.xa1 - cols.xa0;
-  const int ix = (int)blockIdx.y < na ? cols.xa0 + (int)blockIdx.y : cols.xb0 + ((int)blockIdx.y - na);
+  const int by = cols.rev ? (int)gridDim.y - 1 - (int)blockIdx.y : (int)blockIdx.y;
+  const int ix = by < na ? cols.xa0 + by : cols.xb0 + (by - na);
   const bool border = ix < 2 * H || ix >= g.lx;
   const bool peer_wait = h.waitL != nullptr && border;
   if (peer_wait) {  // block-uniform
