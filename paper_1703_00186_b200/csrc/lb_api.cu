@@ -135,7 +135,8 @@ struct lb_ctx {
   uint64_t peer_step = 0;     // steps completed since lb_set_peers
   bool mon_on = false;        // fused monitors (lb_monitor)
   bool mon_valid = false;     // d_mon describes the current A
-  double* d_mon = nullptr;    // monitor_slots x 5 partials
+  double* d_mon = nullptr;    // monitor_slots x 5 partials, then MON_REDUCE_MAX_BLOCKS x 5 (reduce scratch)
+  unsigned int* d_ticket = nullptr;        // k_monitor_reduce arrival counter (kept zero)
   unsigned int* d_status = nullptr;        // peer watchdog flag (device)
   unsigned long long peer_timeout_ns = 20000000000ull;
   lbk::TmaMaps* tma = nullptr;  // tensor maps of f_a / f_b (TMA propagate)
@@ -584,6 +585,7 @@ void lb_destroy(lb_ctx* c) {
   if (c->s_comm) cudaStreamDestroy(c->s_comm);
   if (c->d_part) cudaFree(c->d_part);
   if (c->d_mon) cudaFree(c->d_mon);
+  if (c->d_ticket) cudaFree(c->d_ticket);
   if (c->d_status) cudaFree(c->d_status);
   if (c->tma) lbk::tma_destroy(c->tma);
   graph_reset(c);
@@ -840,19 +842,36 @@ int lb_peek(lb_ctx* c, int which, double* host_out) {
   return lb_peek_cols(c, which, 0, c->g.lx, host_out);
 }
 
+// Device address under which host_dst can be written by a kernel (pinned /
+// registered host memory under UVA), else nullptr.
+static double* host_mapped(double* host_dst) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, host_dst) != cudaSuccess) {
+    cudaGetLastError();  // pageable memory on older runtimes: clear the sticky-free error
+    return nullptr;
+  }
+  return a.type == cudaMemoryTypeHost ? static_cast<double*>(a.devicePointer) : nullptr;
+}
+
 // Enqueue the invariants of A (fused-monitor partials when valid, else a full
-// pass), the cross-rank reduction, and their D2H copy to host_dst.
+// pass), the cross-rank reduction, and their delivery to host_dst: written by
+// the final reduction block itself when host_dst is pinned and there is no
+// cross-rank step, else a 40-byte D2H copy.
 static int invariants_enqueue(lb_ctx* c, double* host_dst) {
   double* res = c->d_part + lbk::invariants_scratch(c->g);
+  double* mapped = c->comm ? nullptr : host_mapped(host_dst);
+  double* out = mapped ? mapped : res;
   if (c->mon_valid) {
+    const int64_t nslots = (int64_t)lbk::monitor_slots(c->g);
     TRY(launch(c, "k_monitor_reduce", c->s, 0, [&] {
-      return lbk::launch_monitor_reduce(c->d_mon, (int64_t)lbk::monitor_slots(c->g), res, c->s);
+      return lbk::launch_monitor_reduce(c->d_mon, nslots, c->d_mon + nslots * 5, c->d_ticket, out, c->s);
     }));
   } else {
     TRY(launch(c, "k_invariants", c->s, c->L.sites, [&] {
-      return lbk::launch_invariants(c->g, c->A, c->d_part, res, c->s);
+      return lbk::launch_invariants(c->g, c->A, c->d_part, out, c->s);
     }));
   }
+  if (mapped) return LB_OK;
   if (c->comm) {
     NC(ncclGroupStart());
     NC(ncclAllReduce(res, res, 4, ncclDouble, ncclSum, c->comm, c->s));
@@ -952,8 +971,11 @@ int lb_set_option(lb_ctx* c, int option, int value) {
 int lb_monitor(lb_ctx* c, int enable) {
   if (!c) return fail(LB_EINVAL, "ctx is NULL");
   if (enable && !c->d_mon) {
-    if (cudaMalloc(&c->d_mon, lbk::monitor_slots(c->g) * 5 * sizeof(double)) != cudaSuccess)
+    const size_t n = (lbk::monitor_slots(c->g) + lbk::MON_REDUCE_MAX_BLOCKS) * 5;
+    if (cudaMalloc(&c->d_mon, n * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&c->d_ticket, sizeof(unsigned int)) != cudaSuccess)
       return fail(LB_ENOMEM, "monitor allocation failed");
+    CU(cudaMemsetAsync(c->d_ticket, 0, sizeof(unsigned int), c->s));
   }
   c->mon_on = enable != 0;
   c->mon_valid = false;

@@ -60,7 +60,12 @@ struct Halo {
 cudaError_t launch_step_fused(const Geo& g, const double* A, double* B, int bc, int coll,
                               const lbd::Relax& r, Cols cols, const Halo& h, double* mon, cudaStream_t s);
 size_t monitor_slots(const Geo& g);
-cudaError_t launch_monitor_reduce(const double* mon, int64_t nslots, double* out, cudaStream_t s);
+// Sum of the slots into out[5] (device or host-mapped pointer) in one launch;
+// part: MON_REDUCE_MAX_BLOCKS x 5 doubles of scratch, ticket: a zeroed counter
+// (left zeroed).  Deterministic: fixed block ranges, partials summed in order.
+constexpr int MON_REDUCE_MAX_BLOCKS = 148;
+cudaError_t launch_monitor_reduce(const double* mon, int64_t nslots, double* part, unsigned int* ticket,
+                                  double* out, cudaStream_t s);
 // TMA-staged kernels (lb_tma.cu): tensor maps of both buffers, built once.
 // Buffer k viewed as {nyp rows, 37 populations, nx columns}, box {256, 1, 1}.
 struct TmaMaps {

@@ -571,8 +571,6 @@ cudaError_t launch_step_fused(const Geo& g, const double* A, double* B, int bc, 
   return cudaGetLastError();
 }
 
-cudaError_t launch_monitor_reduce(const double* mon, int64_t nslots, double* out, cudaStream_t s);
-
 // Step signal of peer mode: this rank's counter += 1 (only this rank writes
 // it; system-scope release), after the fused kernel (stream order) and its
 // border blocks' system fences.
@@ -742,8 +740,60 @@ cudaError_t launch_invariants(const Geo& g, const double* A, double* partials, d
   return cudaGetLastError();
 }
 
-cudaError_t launch_monitor_reduce(const double* mon, int64_t nslots, double* out, cudaStream_t s) {
-  k_invariants_final<<<1, RED_TPB, 0, s>>>(mon, (int)nslots, out);
+// Sum of the fused-monitor slots in ONE launch: block b reduces the fixed slot
+// range [b*chunk, (b+1)*chunk) (one slot per thread at 1920x2048), writes its
+// partial, and the last block to arrive (ticket) sums the partials in block
+// order — so the result is deterministic and no single block walks all slots
+// (a one-block pass over 30k slots cost 56 us per step).
+__global__ void __launch_bounds__(RED_TPB) k_monitor_reduce(const double* __restrict__ mon, int nslots,
+                                                            double* part, unsigned int* ticket,
+                                                            double* out) {
+  __shared__ double sm[5 * RED_TPB];
+  __shared__ bool last;
+  const int t = threadIdx.x;
+  const int chunk = (nslots + (int)gridDim.x - 1) / (int)gridDim.x;
+  const int lo = (int)blockIdx.x * chunk, hi = min(lo + chunk, nslots);
+  double v[5] = {0.0, 0.0, 0.0, 0.0, INFINITY};
+  for (int b = lo + t; b < hi; b += RED_TPB) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] += mon[(int64_t)b * 5 + k];
+    const double m = mon[(int64_t)b * 5 + 4];
+    v[4] = (m != m || m == -INFINITY) ? -INFINITY : fmin(v[4], m);
+  }
+  block_reduce5(v, sm);
+  if (t == 0) {
+#pragma unroll
+    for (int k = 0; k < 5; ++k) part[(int64_t)blockIdx.x * 5 + k] = v[k];
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double w[5] = {0.0, 0.0, 0.0, 0.0, INFINITY};
+  for (int b = t; b < (int)gridDim.x; b += RED_TPB) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) w[k] += __ldcg(part + (int64_t)b * 5 + k);
+    const double m = __ldcg(part + (int64_t)b * 5 + 4);
+    w[4] = (m != m || m == -INFINITY) ? -INFINITY : fmin(w[4], m);
+  }
+  __syncthreads();  // sm reused
+  block_reduce5(w, sm);
+  if (t == 0) {
+#pragma unroll
+    for (int k = 0; k < 5; ++k) out[k] = w[k];
+    *ticket = 0u;  // ready for the next launch (stream-ordered)
+  }
+}
+
+static int monitor_reduce_blocks(int64_t nslots) {
+  const int64_t b = (nslots + RED_TPB - 1) / RED_TPB;
+  return (int)(b < 1 ? 1 : (b > MON_REDUCE_MAX_BLOCKS ? MON_REDUCE_MAX_BLOCKS : b));
+}
+
+cudaError_t launch_monitor_reduce(const double* mon, int64_t nslots, double* part, unsigned int* ticket,
+                                  double* out, cudaStream_t s) {
+  k_monitor_reduce<<<monitor_reduce_blocks(nslots), RED_TPB, 0, s>>>(mon, (int)nslots, part, ticket, out);
   return cudaGetLastError();
 }
 

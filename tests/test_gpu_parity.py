@@ -458,6 +458,33 @@ def test_invariants_async_matches_sync(lb):
     assert np.array_equal(out[:3].numpy(), np.array(sync_vals))
 
 
+@pytest.mark.parametrize("lx,ly", [(7, 6), (300, 2048), (2400, 2048)])
+def test_monitor_reduce_multiblock(lb, lx, ly):
+    """The one-launch slot reduction (1, 19 and the capped 148 blocks): equal to
+    the full pass to rounding, deterministic across calls (ticket reset), and
+    the same whether delivered into pinned memory (written by the kernel) or
+    into a pageable array (D2H copy)."""
+    g = lb.Lattice(lx, ly)
+    g.init_macro(*lbgen.rt_macro(lx, ly, oracle.t0()))
+    g.monitor(True)
+    g.step(1)
+    pinned = torch.zeros((3, 5), dtype=torch.float64).pin_memory()
+    pageable = np.zeros((2, 5))
+    for k in range(3):
+        g.invariants_async(pinned[k])
+    for k in range(2):
+        g.invariants_async(pageable[k])
+    g.sync()
+    p = pinned.numpy()
+    assert np.array_equal(p[0], p[1]) and np.array_equal(p[0], p[2])
+    assert np.array_equal(pageable[0], p[0]) and np.array_equal(pageable[1], p[0])
+    g.monitor(False)
+    full = g.invariants()
+    assert np.allclose(p[0, :4], full[:4], rtol=1e-13, atol=1e-13 * full[0])
+    assert p[0, 4] == full[4]
+    g.close()
+
+
 @pytest.mark.parametrize("overlap,nccl", [(False, False), (True, True)])
 def test_fused_monitors(lb, overlap, nccl):
     """Monitored fused steps leave the state bit-identical, and the in-kernel
