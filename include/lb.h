@@ -222,6 +222,17 @@ int lb_set_stream(lb_ctx* ctx, void* stream);
 int lb_init_macro(lb_ctx* ctx, const double* rho, const double* ux,
                   const double* uy, const double* T, int on_device);
 
+/* A := f_eq of the isobaric Rayleigh-Taylor state of DESIGN.md §4 (the
+ * benchmark workload), evaluated on the device for this
+ * rank's columns: interface y_i(x) = (Ly-1)/2 + max(1, Ly/64) cos(2 pi x /
+ * Lx_tot) + eps[x] (x global), T = t_ref (1 + amp tanh((y_i - y)/width)),
+ * rho = t_ref / T, u = 0.  eps: lx_total doubles, host or device memory (the
+ * caller draws them; lbgen draws U(-1/4, 1/4) from PCG64).  Equals
+ * lb_init_macro on the host-evaluated fields up to the last-ulp differences
+ * of device cos/tanh.  Needs t_ref > 0, width > 0, |amp| < 1 (LB_EINVAL).
+ * Uses B as staging and re-zeroes it.  Only at a step boundary. */
+int lb_init_rt(lb_ctx* ctx, const double* eps, double t_ref, double amp, double width);
+
 /* A := populations given in canonical local layout [37][Lx][Ly] (host memory
  * if on_device == 0, else device).  Only at a step boundary. */
 int lb_set_state(lb_ctx* ctx, const double* canon, int on_device);

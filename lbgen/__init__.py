@@ -29,8 +29,7 @@ def rt_macro(lx_tot: int, ly: int, t_ref: float, seed: int = RT_SEED,
     Returns (rho, ux, uy, T), each float64 [lx][ly] (iy fastest)."""
     if lx is None:
         lx = lx_tot - x0
-    rng = np.random.Generator(np.random.PCG64(seed))
-    eps = rng.uniform(-0.25, 0.25, size=lx_tot)
+    eps = rt_eps(lx_tot, seed)
     x = np.arange(x0, x0 + lx, dtype=np.float64)
     A = max(1.0, ly / 64.0)
     yi = (ly - 1) / 2.0 + A * np.cos(2.0 * np.pi * x / lx_tot) + eps[x0:x0 + lx]
@@ -40,6 +39,13 @@ def rt_macro(lx_tot: int, ly: int, t_ref: float, seed: int = RT_SEED,
     ux = np.zeros_like(T)
     uy = np.zeros_like(T)
     return (np.ascontiguousarray(rho), ux, uy, np.ascontiguousarray(T))
+
+
+def rt_eps(lx_tot: int, seed: int = RT_SEED):
+    """The per-column interface jitter eps_x ~ U(-1/4, 1/4) of rt_macro, for
+    all lx_tot global columns (what lb_init_rt takes)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    return rng.uniform(-0.25, 0.25, size=lx_tot)
 
 
 def perturbed_macro(lx: int, ly: int, t_ref: float, seed: int = 7,

@@ -630,6 +630,22 @@ int lb_init_macro(lb_ctx* c, const double* rho, const double* ux, const double* 
   return LB_OK;
 }
 
+int lb_init_rt(lb_ctx* c, const double* eps, double t_ref, double amp, double width) {
+  TRY(check_boundary(c, "lb_init_rt"));
+  if (!eps) return fail(LB_EINVAL, "NULL eps");
+  if (!(t_ref > 0.0) || !(width > 0.0) || !(std::fabs(amp) < 1.0))
+    return fail(LB_EINVAL, "need t_ref > 0, width > 0, |amp| < 1 (T > 0)");
+  const int lx_total = c->p.lx_total;
+  CU(cudaMemcpyAsync(c->B, eps, lx_total * sizeof(double), cudaMemcpyDefault, c->s));
+  c->halo_fresh = false;
+  c->mon_valid = false;
+  TRY(launch(c, "k_init_rt", c->s, c->L.sites, [&] {
+    return lbk::launch_init_rt(c->g, c->A, c->B, lx_total, c->rank * c->g.lx, t_ref, amp, width, c->s);
+  }));
+  CU(cudaMemsetAsync(c->B, 0, c->L.bytes, c->s));
+  return LB_OK;
+}
+
 int lb_set_state(lb_ctx* c, const double* canon, int on_device) {
   TRY(check_boundary(c, "lb_set_state"));
   if (!canon) return fail(LB_EINVAL, "NULL state");

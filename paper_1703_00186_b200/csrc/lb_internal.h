@@ -83,6 +83,8 @@ cudaError_t launch_peer_pull(const Geo& g, double* A, const double* left_A, cons
                              cudaStream_t s);
 cudaError_t launch_init_macro(const Geo& g, double* A, const double* rho, const double* ux,
                               const double* uy, const double* T, cudaStream_t s);
+cudaError_t launch_init_rt(const Geo& g, double* A, const double* eps, int lx_total, int x0, double t_ref,
+                           double amp, double width, cudaStream_t s);
 cudaError_t launch_canon_to_internal(const Geo& g, const double* canon, double* A, cudaStream_t s);
 cudaError_t launch_internal_to_canon(const Geo& g, const double* A, double* canon, cudaStream_t s);
 // partials: scratch of at least invariants_scratch(g) doubles; out: 5 doubles on device

@@ -632,6 +632,31 @@ cudaError_t launch_init_macro(const Geo& g, double* A, const double* rho, const 
   return cudaGetLastError();
 }
 
+// Rayleigh-Taylor initial state on the device (lb_init_rt): the recipe of
+// DESIGN.md §4 evaluated per site, then A := f_eq.  eps: the lx_total column
+// jitters (device), x0: this rank's first global column.
+__global__ void __launch_bounds__(TPB) k_init_rt(double* __restrict__ A, Geo g,
+                                                 const double* __restrict__ eps, int lx_total, int x0,
+                                                 double t_ref, double amp, double width) {
+  const int y = blockIdx.x * TPB + threadIdx.x;
+  const int x = blockIdx.y;
+  if (y >= g.ly) return;
+  const int xg = x0 + x;
+  const double ampl = fmax(1.0, g.ly / 64.0);
+  const double yi = (g.ly - 1) / 2.0 + ampl * cos(2.0 * M_PI * (double)xg / (double)lx_total) + eps[xg];
+  const double T = t_ref * (1.0 + amp * tanh((yi - (double)y) / width));
+  double f[Q];
+  feq_site(t_ref / T, 0.0, 0.0, T, f);
+  store_site(A, g, H + x, y, f);
+}
+
+cudaError_t launch_init_rt(const Geo& g, double* A, const double* eps, int lx_total, int x0, double t_ref,
+                           double amp, double width, cudaStream_t s) {
+  dim3 grid((g.ly + TPB - 1) / TPB, g.lx);
+  k_init_rt<<<grid, TPB, 0, s>>>(A, g, eps, lx_total, x0, t_ref, amp, width);
+  return cudaGetLastError();
+}
+
 // canonical [37][lx][ly] <-> internal physical sites
 __global__ void k_canon_to_internal(const double* __restrict__ C, double* __restrict__ A, Geo g) {
   const int y = blockIdx.x * blockDim.x + threadIdx.x;

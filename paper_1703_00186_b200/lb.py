@@ -26,7 +26,7 @@ SO_PATH = os.path.join(_HERE, "liblb_d2q37.so")
 
 # every symbol include/lb.h declares
 EXPORTS = ["lb_query_layout", "lb_exchange_plan", "lb_constants", "lb_kwall", "lb_nccl_unique_id", "lb_last_error",
-           "lb_strerror", "lb_init", "lb_destroy", "lb_get_layout", "lb_set_stream", "lb_init_macro",
+           "lb_strerror", "lb_init", "lb_destroy", "lb_get_layout", "lb_set_stream", "lb_init_macro", "lb_init_rt",
            "lb_set_state", "lb_exchange", "lb_propagate", "lb_bc", "lb_collide", "lb_step",
            "lb_gather", "lb_peek", "lb_invariants", "lb_sync", "lb_profile_enable",
            "lb_profile_reset", "lb_profile_read", "lb_launch_count", "lb_set_peers",
@@ -103,6 +103,7 @@ def lib():
         "lb_get_layout": (i, [vp, p(lb_layout)]),
         "lb_set_stream": (i, [vp, vp]),
         "lb_init_macro": (i, [vp, vp, vp, vp, vp, i]),
+        "lb_init_rt": (i, [vp, vp, d, d, d]),
         "lb_set_state": (i, [vp, vp, i]),
         "lb_exchange": (i, [vp]), "lb_propagate": (i, [vp]), "lb_bc": (i, [vp]),
         "lb_collide": (i, [vp]), "lb_step": (i, [vp, i]),
@@ -261,6 +262,14 @@ class Lattice:
                 assert a.size == self.sites
             _check(lib().lb_init_macro(self._ctx, *[_dptr(a) for a in arrs], 0))
             self.sync()
+
+    def init_rt(self, eps, t_ref: float, amp: float = 0.05, width: float = 2.0):
+        """Rayleigh-Taylor initial state evaluated on the device (lb_init_rt);
+        eps: the lx_total column jitters (lbgen.rt_eps)."""
+        e = np.ascontiguousarray(np.asarray(eps, dtype=np.float64))
+        assert e.size == self.params.lx_total
+        _check(lib().lb_init_rt(self._ctx, _dptr(e), float(t_ref), float(amp), float(width)))
+        self.sync()
 
     def set_state(self, canon):
         import torch

@@ -458,6 +458,29 @@ def test_invariants_async_matches_sync(lb):
     assert np.array_equal(out[:3].numpy(), np.array(sync_vals))
 
 
+# ------------------------------------------------------------------ device RT init
+
+@pytest.mark.parametrize("lx,ly", [(64, 32), (96, 200)])
+def test_init_rt_matches_host_fields(lb, lx, ly):
+    """lb_init_rt (recipe evaluated on the device) = f_eq of lbgen.rt_macro's
+    host fields (oracle init) up to device cos/tanh rounding, and its X slabs
+    are the columns of the 1-slab state bit for bit (global column index)."""
+    g = lb.Lattice(lx, ly)
+    g.init_rt(lbgen.rt_eps(lx), oracle.t0())
+    o = oracle.Lattice(lx, ly)
+    o.init_macro(*lbgen.rt_macro(lx, ly, oracle.t0()))
+    full = g.peek(0)
+    assert max_rel(full, o.get_state(0)) < 1e-13
+    h = lx // 2
+    s1 = lb.Lattice(lx, ly, rank=1, nranks=2)
+    s1.init_rt(lbgen.rt_eps(lx), oracle.t0())
+    assert np.array_equal(s1.peek(0), full[:, h:, :])
+    with pytest.raises(lb.LBError):
+        g.init_rt(lbgen.rt_eps(lx), -1.0)
+    for x in (g, s1):
+        x.close()
+
+
 @pytest.mark.parametrize("lx,ly", [(7, 6), (300, 2048), (2400, 2048)])
 def test_monitor_reduce_multiblock(lb, lx, ly):
     """The one-launch slot reduction (1, 19 and the capped 148 blocks): equal to
