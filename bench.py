@@ -185,10 +185,12 @@ def kernel_passes(lb, lx_total, ly, fields, hbm_peak, fp64_peak, ncu, nsteps=10)
     regularised steps on the same workload (library instrumentation)."""
     kern = {}
     for mode, coll, impl in (("split", "bgk", "ldg"), ("split", "bgk", "tma"), ("fused", "bgk", "tma"),
-                             ("fused", "regularized", "ldg"), ("split", "regularized", "ldg")):
+                             ("fused", "regularized", "ldg"), ("split", "regularized", "ldg"), ("fused", "bgk", "tb")):
         g = lb.Lattice(lx_total, ly, mode=mode, collision=coll)
         if mode == "split":
             g.set_propagate_impl(impl)
+        elif impl == "tb":
+            g.temporal(True)  # two steps per launch (k_step2_tb), an option: see DESIGN.md §8
         else:
             g.set_fused_impl(impl)
         g.init_macro(*fields)
@@ -216,9 +218,17 @@ def kernel_passes(lb, lx_total, ly, fields, hbm_peak, fp64_peak, ncu, nsteps=10)
                     e.update({"flops_per_site_ncu": fl, "fp64_tflops": tf, "fp64_frac": tf / fp64_peak,
                               "fp64_peak_tflops": fp64_peak})
                 e["paper_convention_6500_flop_tflops"] = 6500 * e["mlups"] * 1e6 / 1e12
+            if k == "k_step2_tb":
+                # one launch = two time steps; algorithmic HBM traffic = one read + one
+                # write of the state (592 B/site) per launch
+                e["site_updates_per_launch"] = v["units"] / v["launches"]
+                e["mlups"] = v["units"] / v["launches"] / (avg * 1e-3) / 1e6
+                e["gbs"] = BYTES_PER_SITE * v["units"] / 2 / v["launches"] / (avg * 1e-3) / 1e9
+                e["hbm_frac"] = e["gbs"] / hbm_peak
             kern[k] = e
         step_ms = sum(v["total_ms"] for v in sp.values()) / nsteps
-        kern[f"{mode}_{coll}" + ("_tma" if impl == "tma" else "") + "_step_mlups"] = lx_total * ly / (step_ms * 1e-3) / 1e6
+        kern[f"{mode}_{coll}" + ("_" + impl if impl in ("tma", "tb") else "") + "_step_mlups"] = \
+            lx_total * ly / (step_ms * 1e-3) / 1e6
     return kern
 
 

@@ -308,7 +308,21 @@ int lb_sync(lb_ctx* ctx);
  * steady state of the fused N = 1 path and of the peer path (bit-identical;
  * fewer host launches, matters for small lattices).  Needs a non-default
  * context stream; ignored while profiling. */
-enum lb_option { LB_OPT_PROPAGATE_IMPL = 0, LB_OPT_FUSED_IMPL = 1, LB_OPT_CUDA_GRAPH = 2 };
+/* LB_OPT_TEMPORAL (value 1): lb_step advances two steps per pass over HBM
+ * where it can (N = 1 without NCCL or peers, walls, fused mode, monitors off):
+ * one launch of the two-step kernel computes states n+1 and n+2, keeping n+1
+ * in shared memory (temporal blocking).  Bit-identical to two
+ * fused steps; an odd remainder takes one fused step.  LB_OPT_TB_GRID: CTAs of
+ * that kernel (0 = one per SM), LB_OPT_TB_L2_PREFETCH: L2 prefetch distance in
+ * columns (0 = off, <= 64). */
+enum lb_option {
+  LB_OPT_PROPAGATE_IMPL = 0,
+  LB_OPT_FUSED_IMPL = 1,
+  LB_OPT_CUDA_GRAPH = 2,
+  LB_OPT_TEMPORAL = 3,
+  LB_OPT_TB_GRID = 4,
+  LB_OPT_TB_L2_PREFETCH = 5
+};
 int lb_set_option(lb_ctx* ctx, int option, int value);
 
 /* Fused monitors.  enable != 0: every fused step also reduces, per block, the

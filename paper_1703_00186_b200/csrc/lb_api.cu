@@ -143,6 +143,11 @@ struct lb_ctx {
   int prop_impl = 0;            // LB_OPT_PROPAGATE_IMPL (1 = TMA when available)
   int fused_impl = 0;           // LB_OPT_FUSED_IMPL (1 = TMA-staged windows)
   bool graph_on = false;        // LB_OPT_CUDA_GRAPH: lb_step replays 2-step graphs
+  lbk::TbMaps* tb = nullptr;    // tensor maps of the two-step kernel (lb_tb.cu)
+  int tb_on = 0;                // LB_OPT_TEMPORAL: two steps per pass where possible
+  int tb_grid = 0;              // LB_OPT_TB_GRID: CTAs of the two-step kernel (0 = SM count)
+  int tb_l2 = 0;                // LB_OPT_TB_L2_PREFETCH: L2 prefetch distance in columns
+  int sm_count = 148;
   cudaGraphExec_t gexec[2] = {nullptr, nullptr};  // keyed by the parity at graph start
   int gkey[2] = {-1, -1};       // configuration each graph was captured for
   int64_t glaunch[2] = {0, 0};  // kernel launches inside each graph
@@ -552,8 +557,13 @@ int lb_init(const lb_params* p, const lb_dist* d, double* f_a, double* f_b, void
     return bail(fail(LB_ECUDA, "constant upload failed"));
   double ginv[lbd::NGINV];
   if (!gram_inverse(ginv)) return bail(fail(LB_EINVAL, "singular Gram matrix"));
-  if (lbk::upload_ginv(ginv, c->s) != cudaSuccess)
+  if (lbk::upload_ginv(ginv, c->s) != cudaSuccess || lbk::tb_upload_constants(kb, kt, ginv, c->s) != cudaSuccess)
     return bail(fail(LB_ECUDA, "constant upload failed"));
+  {
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess)
+      cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, dev);
+  }
   // TMA-staged propagate is the default when the tensor maps encode (B200:
   // 6.62 vs 6.54 TB/s for the register gather); otherwise the gather
   c->tma = lbk::tma_create(c->g, c->A, c->B);
@@ -588,6 +598,7 @@ void lb_destroy(lb_ctx* c) {
   if (c->d_ticket) cudaFree(c->d_ticket);
   if (c->d_status) cudaFree(c->d_status);
   if (c->tma) lbk::tma_destroy(c->tma);
+  if (c->tb) lbk::tb_destroy(c->tb);
   graph_reset(c);
   if (c->h_pin) cudaFreeHost(c->h_pin);
   delete c;
@@ -770,12 +781,34 @@ static int graph_two_steps(lb_ctx* c) {
   return LB_OK;
 }
 
+// Two steps in one pass (lb_tb.cu): N = 1 without NCCL or peers, walls, fused
+// mode, monitors off.  Bit-identical to two fused steps.
+static bool tb_usable(const lb_ctx* c) {
+  return c->tb_on && c->tb && c->nranks == 1 && !c->comm && !c->peers_on && c->p.mode == LB_MODE_FUSED &&
+         c->p.bc_y != LB_PERIODIC && !c->mon_on;
+}
+
+static int step_tb(lb_ctx* c) {
+  const int grid = c->tb_grid > 0 ? c->tb_grid : c->sm_count;
+  TRY(launch(c, c->p.collision ? "k_step2_tb_reg" : "k_step2_tb", c->s, 2 * c->L.sites, [&] {
+    return lbk::launch_step2_tb(c->g, c->tb, c->par, c->B, c->p.bc_y, c->p.collision, c->relax, grid, c->tb_l2,
+                                c->s);
+  }));
+  swap_ab(c);  // B held state n + 2: it becomes A
+  c->halo_fresh = true;  // the kernel stored the border columns into B's halo
+  fused_step_done(c);
+  return LB_OK;
+}
+
 int lb_step(lb_ctx* c, int nsteps) {
   TRY(check_boundary(c, "lb_step"));
   if (nsteps < 0) return fail(LB_EINVAL, "nsteps < 0");
   int k = 0;
   while (k < nsteps) {
-    if (nsteps - k >= 2 && graphable(c)) {
+    if (nsteps - k >= 2 && tb_usable(c)) {
+      TRY(step_tb(c));
+      k += 2;
+    } else if (nsteps - k >= 2 && graphable(c)) {
       TRY(graph_two_steps(c));
       k += 2;
     } else {
@@ -973,6 +1006,22 @@ int lb_set_option(lb_ctx* c, int option, int value) {
       if (value && !c->s) return fail(LB_EINVAL, "CUDA graphs need a non-default context stream");
       c->graph_on = value != 0;
       if (!c->graph_on) graph_reset(c);
+      return LB_OK;
+    case LB_OPT_TEMPORAL:
+      if (value != 0 && value != 1) return fail(LB_EINVAL, "temporal blocking must be 0 or 1");
+      if (value == 1 && !c->tb) {
+        c->tb = lbk::tb_create(c->g, c->par ? c->B : c->A, c->par ? c->A : c->B);
+        if (!c->tb) return fail(LB_ECUDA, "two-step kernel unavailable (tensor maps or lx < 6)");
+      }
+      c->tb_on = value;
+      return LB_OK;
+    case LB_OPT_TB_GRID:
+      if (value < 0) return fail(LB_EINVAL, "grid must be >= 0");
+      c->tb_grid = value;
+      return LB_OK;
+    case LB_OPT_TB_L2_PREFETCH:
+      if (value < 0 || value > 64) return fail(LB_EINVAL, "L2 prefetch distance must be in [0, 64]");
+      c->tb_l2 = value;
       return LB_OK;
     case LB_OPT_FUSED_IMPL:
       if (value != 0 && value != 1) return fail(LB_EINVAL, "fused impl must be 0 (gather) or 1 (TMA)");

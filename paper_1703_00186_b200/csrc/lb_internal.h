@@ -77,6 +77,21 @@ cudaError_t launch_propagate_tma(const Geo& g, const TmaMaps* t, int src_buf, do
 // Fused step with TMA-staged windows (N = 1 local wrap path; walls only)
 cudaError_t launch_step_fused_tma(const Geo& g, const TmaMaps* t, int src_buf, const double* A, double* B,
                                   int bc, int coll, const lbd::Relax& r, const Halo& h, cudaStream_t s);
+// Two steps per pass (lb_tb.cu, temporal blocking): N = 1, walls only.  The
+// state-n windows are loaded by TMA straight from the physical columns
+// (periodic wrap in the coordinates), so A's halo is not read; B's halo is
+// written (the next step's wrap).
+struct TbMaps {
+  CUtensorMap load[2];  // per-population windows, box {HT + 8, 1, 1}
+  CUtensorMap pf[2];    // L2 prefetch of a column window, box {HT + 16, 37, 1}
+};
+TbMaps* tb_create(const Geo& g, double* buf0, double* buf1);
+void tb_destroy(TbMaps* t);
+// lb_tb.cu's own copies of the wall constants and the Gram inverse
+cudaError_t tb_upload_constants(const double* k_bottom, const double* k_top, const double* ginv, cudaStream_t s);
+// grid: CTAs (one per SM); l2_dist: L2 prefetch distance in columns (0 = off)
+cudaError_t launch_step2_tb(const Geo& g, const TbMaps* t, int src_buf, double* B, int bc, int coll,
+                            const lbd::Relax& r, int grid, int l2_dist, cudaStream_t s);
 // this rank's counter += 1 (system-scope release), after the step kernel
 cudaError_t launch_signal(unsigned long long* done, cudaStream_t s);
 cudaError_t launch_peer_pull(const Geo& g, double* A, const double* left_A, const double* right_A,

@@ -1,0 +1,401 @@
+// lb_tb.cu — two time steps per pass over HBM (temporal blocking of the fused
+// pull step, §8a5 extended; DESIGN.md §6 "k_step2_tb").
+//
+// The fused step (k_step_fused) moves 592 B/site per step and runs at the HBM
+// copy roof, with the FP64 pipe ~25 % busy.  This kernel computes steps n+1 AND
+// n+2 from state n in one pass, keeping the intermediate state n+1 in shared
+// memory, so HBM sees ~296·(1 + overlap) B read + 296 B written per site per
+// TWO steps.  The per-site arithmetic is the very same device code as the fused
+// kernel (gather order, thermal_wall, collide_site / collide_site_reg), so the
+// result is bit-identical to two k_step_fused launches.
+//
+// Tiling.  A CTA owns a strip of HT rows [ya, ya+HT) and sweeps a range of
+// output columns [xs, xe) in x.  Iteration t of a sweep:
+//   * TMA (one elected thread) loads state-n column k = t + PF (sweep index;
+//     global column xs - 6 + k, wrapped periodically — N = 1 needs no halo):
+//     for every population l the rows [ya - 3 - cy_l, ya + HT + 3 - cy_l) it
+//     will be pulled from, rounded out to a 16-byte box start (the TMA
+//     alignment rule, tools/tma_probe.cu) — R0 = HT + 8 rows;
+//   * phase 1 (warps [0, NW1)): step n+1 at column c1 = xs - 9 + t for the
+//     R1 = HT + 6 rows [ya - 3, ya + HT + 3) (the ±3-row apron step n+2 pulls
+//     from), gathered from the state-n ring, written to the state-(n+1) ring;
+//   * phase 2 (warps [NW1, NW1+NW2)): step n+2 at column c2 = xs - 13 + t for
+//     the HT rows of the strip, gathered from the state-(n+1) ring, stored to B
+//     (and, for the 3+3 border columns, into B's halo: the next step's wrap).
+// Both phases of an iteration are independent (phase 2 lags by one extra
+// column), so ONE __syncthreads per iteration orders everything.
+//
+// Rings.  Population l of a column is pulled by the output column x + cx_l, so
+// it lives cx_l + 3 iterations after arrival: the state-n ring of population l
+// has L0 = cx_l + 4 + PF slots (PF = TMA prefetch depth), the state-(n+1) ring
+// L1 = cx_l + 5.  Summed over the 37 populations that is 37·(4+PF) and 37·5
+// column slots instead of 7 + 7 full columns.  State-n slots are padded to
+// 128 bytes (TMA destination alignment).  HT = 56, PF = 3: 224 KB smem.
+//
+// Walls (G9): the strips next to a wall pull mirrored populations (REFL(l) at
+// the image row) from the same rings — every image row lies inside the window
+// loaded for REFL(l); warps whose rows are all >= 3 rows from both walls take
+// the mirror-free path (warp-uniform).  Periodic-Y geometry is not supported
+// here (the 1-step kernel serves it).
+//
+// Work split: the strips × lx column-units are cut into gridDim.x contiguous
+// ranges (one CTA per SM, persistent); a range crossing a strip boundary is two
+// sweeps.  A strip that would pass the top wall is moved down to end on it
+// (rows computed twice produce identical values).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "lb_collide.cuh"
+#include "lb_device.cuh"
+#include "lb_internal.h"
+
+namespace lbk {
+using namespace lbd;
+
+namespace {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// relative start row (to ya) of population l's state-n window: -3 - cy_l,
+// lowered by one when that is odd (box starts must be 16-byte aligned; ya and
+// y0 are even)
+LB_HD constexpr int A0(int l) { return -3 - CY(l) - ((CY(l) + 1) & 1); }
+
+template <int PF>
+LB_HD constexpr int L0(int l) { return CX(l) + 4 + PF; }
+LB_HD constexpr int L1(int l) { return CX(l) + 5; }
+
+// Literal tables (a constexpr loop evaluated in device code is NOT folded by
+// cicc: it materialises the velocity table on the stack, and inside this
+// kernel's loops it made the compile time explode).  CXSUM(l) = sum_{m<l} cx_m;
+// REFL(l) = refl(l).  Both are checked against lb_device.cuh by static_assert.
+LB_HD constexpr int CXSUM(int l) {
+  constexpr int t[Q + 1] = {0,  3,  6,  9,  11, 13, 15, 17, 19, 20, 21, 22, 23, 24, 25, 26, 26, 26, 26,
+                            26, 26, 26, 26, 25, 24, 23, 22, 21, 20, 19, 17, 15, 13, 11, 9,  6,  3,  0};
+  return t[l];
+}
+LB_HD constexpr int REFL(int l) {
+  constexpr int t[Q] = {2,  1,  0,  7,  6,  5,  4,  3,  14, 13, 12, 11, 10, 9,  8,  21, 20, 19, 18,
+                        17, 16, 15, 28, 27, 26, 25, 24, 23, 22, 33, 32, 31, 30, 29, 36, 35, 34};
+  return t[l];
+}
+constexpr bool tables_ok() {
+  int s = 0;
+  for (int l = 0; l < Q; ++l) {
+    if (CXSUM(l) != s || REFL(l) != refl(l)) return false;
+    s += CX(l);
+  }
+  return CXSUM(Q) == s;
+}
+static_assert(tables_ok(), "CXSUM / REFL tables");
+
+// ring slots of the populations before l (state n, state n+1)
+template <int PF>
+LB_HD constexpr int SLOTS0_BEFORE(int l) { return CXSUM(l) + (4 + PF) * l; }
+LB_HD constexpr int SLOTS1_BEFORE(int l) { return CXSUM(l) + 5 * l; }
+
+template <int HT_, int PF_>
+struct TbCfg {
+  static constexpr int HT = HT_;
+  static constexpr int PF = PF_;
+  static constexpr int R0 = HT + 8;                 // TMA box rows of a state-n window
+  static constexpr int P0 = (R0 + 15) / 16 * 16;    // slot pitch: TMA smem destinations are 128-byte aligned
+  static constexpr int R1 = HT + 6;
+  static constexpr int NW1 = (R1 + 31) / 32;
+  static constexpr int NW2 = (HT + 31) / 32;
+  static constexpr int NT = 32 * (NW1 + NW2 + 1);  // + the TMA producer warp
+  static constexpr int NB = PF + 1;  // mbarriers (columns in flight + the one being consumed)
+  static constexpr int S0_DBL = SLOTS0_BEFORE<PF>(Q) * P0;
+  static constexpr int S1_DBL = SLOTS1_BEFORE(Q) * R1;
+  static constexpr size_t SMEM = (size_t)(S0_DBL + S1_DBL) * sizeof(double) + NB * sizeof(uint64_t);
+  static_assert(R0 % 2 == 0 && R0 <= 256, "TMA box rows");
+  static_assert(SMEM <= 232448, "shared memory per CTA");
+};
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+// An opaque copy of a loop-invariant value: keeps the compiler from hoisting
+// the 37 per-population store addresses out of the sweep loop (37 live 64-bit
+// registers on top of the 37 populations).
+__device__ __forceinline__ int opaque(int v) {
+  int r;
+  asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+  return r;
+}
+
+// periodic wrap of an internal column index into the physical range [3, 3+lx)
+__device__ __forceinline__ int wrap_col(int j, int lx) {
+  int x = j - H;
+  if (x < 0) x += lx;
+  else if (x >= lx) x -= lx;
+  return H + x;
+}
+
+// Phase 1 site update: state n+1 at row y = ya - 3 + i from the state-n ring
+// (iteration t), result into the state-(n+1) ring.  MIRROR: rows within 3 of
+// a wall (the warp-uniform non-interior path).
+template <int BC, int COLL, int PF, int P0, int R1, bool MIRROR>
+__device__ __forceinline__ void phase1(const double* s0, double* s1, int t, int i, int y, int ya, int ly,
+                                       const Relax& r) {
+  double f[Q];
+  const int io = opaque(i);  // not hoistable: no per-population address registers
+#pragma unroll
+  for (int l = 0; l < Q; ++l) {
+    // REFL(l) has the same cx, so the same ring slot index
+    const int slot = (t - 3 - CX(l)) % L0<PF>(l);
+    int off = SLOTS0_BEFORE<PF>(l) * P0 + io - 3 - CY(l) - A0(l);
+    if (MIRROR) {
+      const int sy = y - CY(l);
+      if (sy < 0) off = SLOTS0_BEFORE<PF>(REFL(l)) * P0 + (-1 - sy) - ya - A0(REFL(l));
+      else if (sy >= ly) off = SLOTS0_BEFORE<PF>(REFL(l)) * P0 + (2 * ly - 1 - sy) - ya - A0(REFL(l));
+    }
+    f[l] = s0[slot * P0 + off];
+  }
+  if (MIRROR && BC == BC_THERMAL && (y < 3 || y >= ly - 3)) thermal_wall(f, y < 3 ? 0 : 1);
+  if (COLL == COLL_REGULARIZED) collide_site_reg(f, r);
+  else collide_site(f, r);
+#pragma unroll
+  for (int l = 0; l < Q; ++l) s1[(SLOTS1_BEFORE(l) + (t % L1(l))) * R1 + io] = f[l];
+}
+
+// Phase 2 site update: state n+2 at row y = ya + i, column c2, from the
+// state-(n+1) ring, stored to B (+ B's halo for the 3+3 border columns).
+template <int BC, int COLL, int R1, bool MIRROR>
+__device__ __forceinline__ void phase2(const double* s1, double* __restrict__ B, const Geo& g, int t, int i,
+                                       int y, int ya, int c2, const Relax& r) {
+  const int ly = g.ly;
+  double f[Q];
+  const int io = opaque(i);
+#pragma unroll
+  for (int l = 0; l < Q; ++l) {
+    const int slot = (t - 4 - CX(l)) % L1(l);
+    int off = SLOTS1_BEFORE(l) * R1 + io + 3 - CY(l);
+    if (MIRROR) {
+      const int sy = y - CY(l);
+      if (sy < 0) off = SLOTS1_BEFORE(REFL(l)) * R1 + (-1 - sy) - ya + 3;
+      else if (sy >= ly) off = SLOTS1_BEFORE(REFL(l)) * R1 + (2 * ly - 1 - sy) - ya + 3;
+    }
+    f[l] = s1[slot * R1 + off];
+  }
+  if (MIRROR && BC == BC_THERMAL && (y < 3 || y >= ly - 3)) thermal_wall(f, y < 3 ? 0 : 1);
+  if (COLL == COLL_REGULARIZED) collide_site_reg(f, r);
+  else collide_site(f, r);
+  const int nyp = opaque(g.nyp);
+  double* p = B + (int64_t)c2 * g.cs + g.y0 + y;
+#pragma unroll
+  for (int l = 0; l < Q; ++l) p[l * nyp] = f[l];
+  // N = 1 wrap of the next step: border columns also go to the halo
+  if (c2 < 2 * H) {
+    double* q = p + (int64_t)g.lx * g.cs;
+#pragma unroll
+    for (int l = 0; l < Q; ++l) q[l * nyp] = f[l];
+  }
+  if (c2 >= g.lx) {
+    double* q = p - (int64_t)g.lx * g.cs;
+#pragma unroll
+    for (int l = 0; l < Q; ++l) q[l * nyp] = f[l];
+  }
+}
+
+// Warps [0, NW1): phase 1; [NW1, NW1 + NW2): phase 2; the last warp is the
+// TMA producer (its lane 0 issues the 37 window loads of a column while the
+// compute warps work, so the issue cost is off their critical path).
+template <int BC, int COLL, int HT, int PF>
+__global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
+    k_step2_tb(const __grid_constant__ CUtensorMap src, const __grid_constant__ CUtensorMap pf_map,
+               double* __restrict__ B, Geo g, Relax r, int nstrips, int l2_dist) {
+  using C = TbCfg<HT, PF>;
+  constexpr int R0 = C::R0, P0 = C::P0, R1 = C::R1, NB = C::NB;
+  extern __shared__ __align__(128) double sm[];
+  double* s0 = sm;
+  double* s1 = sm + C::S0_DBL;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + C::S0_DBL + C::S1_DBL);
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int lx = g.lx, ly = g.ly;
+  const bool producer = tid == 32 * (C::NW1 + C::NW2);
+
+  if (producer) {
+    for (int i = 0; i < NB; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bars + i)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const int64_t U = (int64_t)nstrips * lx;
+  int64_t u = U * blockIdx.x / gridDim.x;
+  const int64_t u_end = U * (blockIdx.x + 1) / gridDim.x;
+  uint32_t kglob = 0;  // columns loaded by this CTA over all its sweeps (barrier phase)
+
+  while (u < u_end) {
+    const int strip = (int)(u / lx);
+    const int x0 = (int)(u % lx);
+    const int x1 = (int)std::min<int64_t>(lx, x0 + (u_end - u));
+    u += x1 - x0;
+    const int xs = H + x0, W = x1 - x0;  // output columns [xs, xs + W)
+    // strip rows [ya, ya + HT); the top strip is moved down to end on the wall,
+    // ya kept even (TMA box starts must be 16-byte aligned): it may then
+    // reach one row past the wall, which is simply not computed
+    const int ya = std::max(0, std::min(strip * HT, (ly - HT + 1) & ~1));
+    const int ncols = W + 12;         // state-n columns of this sweep
+    const int niter = W + 13;         // iterations
+    const int rbase = g.y0 + ya;      // internal row of ya
+
+    auto issue = [&](int k) {         // TMA of sweep column k (producer only)
+      const uint32_t kb = kglob + (uint32_t)k;
+      const uint32_t bar = smem_u32(bars + kb % NB);
+      const int col = wrap_col(xs - 6 + k, lx);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                   "r"((uint32_t)(Q * R0 * sizeof(double))));
+#pragma unroll
+      for (int l = 0; l < Q; ++l) {
+        double* dst = s0 + (SLOTS0_BEFORE<PF>(l) + (k % L0<PF>(l))) * P0;
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+            "l"(&src), "r"(rbase + A0(l)), "r"(l), "r"(col), "r"(bar)
+            : "memory");
+      }
+      if (l2_dist > 0 && k + l2_dist < ncols) {
+        const int pcol = wrap_col(xs - 6 + k + l2_dist, lx);
+        asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(&pf_map),
+                     "r"(rbase - 8), "r"(0), "r"(pcol)
+                     : "memory");
+      }
+    };
+
+    if (producer)
+      for (int k = 0; k < PF && k < ncols; ++k) issue(k);
+
+    for (int t = 0; t < niter; ++t) {
+      __syncthreads();  // every read of iteration t-1 is done: the slots refilled below are free
+      if (warp == C::NW1 + C::NW2) {
+        if (producer && t + PF < ncols) issue(t + PF);
+        continue;
+      }
+      if (t < ncols) {
+        const uint32_t kb = kglob + (uint32_t)t;
+        mbar_wait(smem_u32(bars + kb % NB), (kb / NB) & 1);
+      }
+      if (warp < C::NW1) {
+        // phase 1: state n+1 at column c1 = xs - 9 + t, rows [ya-3, ya+HT+3)
+        const int i = tid;
+        const int y = ya - 3 + i;
+        if (t >= 6 && t < W + 12 && i < R1 && y >= 0 && y < ly) {
+          const int wy0 = ya - 3 + (tid & ~31);
+          if (wy0 >= 3 && wy0 + 32 <= ly - 3)
+            phase1<BC, COLL, PF, P0, R1, false>(s0, s1, t, i, y, ya, ly, r);
+          else
+            phase1<BC, COLL, PF, P0, R1, true>(s0, s1, t, i, y, ya, ly, r);
+        }
+      } else {
+        // phase 2: state n+2 at column c2 = xs - 13 + t, rows [ya, ya+HT)
+        const int i = tid - 32 * C::NW1;
+        const int y = ya + i;
+        if (t >= 13 && i < HT && y < ly) {
+          const int wy0 = ya + (i & ~31);
+          if (wy0 >= 3 && wy0 + 32 <= ly - 3)
+            phase2<BC, COLL, R1, false>(s1, B, g, t, i, y, ya, xs - 13 + t, r);
+          else
+            phase2<BC, COLL, R1, true>(s1, B, g, t, i, y, ya, xs - 13 + t, r);
+        }
+      }
+    }
+    kglob += (uint32_t)ncols;
+    __syncthreads();  // the next sweep refills every ring
+  }
+}
+
+// TMA maps of one buffer: per-population windows (box {R0, 1, 1}) and the
+// whole-column L2 prefetch box {HT + 16, 37, 1}.
+bool encode(CUtensorMap* m, double* base, const Geo& g, int box_rows, int box_pops) {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return false;
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  const cuuint64_t dims[3] = {(cuuint64_t)g.nyp, (cuuint64_t)Q, (cuuint64_t)g.nx};
+  const cuuint64_t strides[2] = {(cuuint64_t)g.nyp * sizeof(double), (cuuint64_t)g.cs * sizeof(double)};
+  const cuuint32_t box[3] = {(cuuint32_t)box_rows, (cuuint32_t)box_pops, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+constexpr int TB_HT = 56;
+constexpr int TB_PF = 3;
+using Cfg = TbCfg<TB_HT, TB_PF>;
+
+template <int BC, int COLL>
+cudaError_t launch_tb(const Geo& g, const TbMaps* t, int src_buf, double* B, const Relax& r, int grid,
+                      int l2_dist, cudaStream_t s) {
+  auto kern = k_step2_tb<BC, COLL, TB_HT, TB_PF>;
+  static unsigned long long done_mask = 0;  // opt-in smem is a per-device attribute
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev >= 64 || !(done_mask >> dev & 1ull)) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
+    if (e != cudaSuccess) return e;
+    if (dev < 64) done_mask |= 1ull << dev;
+  }
+  const int nstrips = (g.ly + TB_HT - 1) / TB_HT;
+  const int64_t U = (int64_t)nstrips * g.lx;
+  const int G = (int)std::min<int64_t>(grid, U);
+  kern<<<G, Cfg::NT, Cfg::SMEM, s>>>(t->load[src_buf], t->pf[src_buf], B, g, r, nstrips, l2_dist);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+TbMaps* tb_create(const Geo& g, double* buf0, double* buf1) {
+  if (g.y0 % 2 || g.nyp % 2 || g.lx < 2 * H) return nullptr;
+  auto* t = new TbMaps();
+  double* bufs[2] = {buf0, buf1};
+  for (int k = 0; k < 2; ++k)
+    if (!encode(&t->load[k], bufs[k], g, Cfg::R0, 1) || !encode(&t->pf[k], bufs[k], g, TB_HT + 16, Q)) {
+      delete t;
+      return nullptr;
+    }
+  return t;
+}
+
+void tb_destroy(TbMaps* t) { delete t; }
+
+cudaError_t tb_upload_constants(const double* k_bottom, const double* k_top, const double* ginv, cudaStream_t s) {
+  cudaError_t e = cudaMemcpyToSymbolAsync(c_kwall, k_bottom, sizeof(double) * Q, 0, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpyToSymbolAsync(c_kwall, k_top, sizeof(double) * Q, sizeof(double) * Q, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpyToSymbolAsync(c_ginv, ginv, sizeof(double) * NGINV, 0, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return e;
+  return cudaStreamSynchronize(s);
+}
+
+cudaError_t launch_step2_tb(const Geo& g, const TbMaps* t, int src_buf, double* B, int bc, int coll,
+                            const Relax& r, int grid, int l2_dist, cudaStream_t s) {
+  if (bc == BC_THERMAL)
+    return coll == COLL_REGULARIZED ? launch_tb<BC_THERMAL, COLL_REGULARIZED>(g, t, src_buf, B, r, grid, l2_dist, s)
+                                    : launch_tb<BC_THERMAL, COLL_BGK>(g, t, src_buf, B, r, grid, l2_dist, s);
+  if (bc == BC_ADIABATIC)
+    return coll == COLL_REGULARIZED
+               ? launch_tb<BC_ADIABATIC, COLL_REGULARIZED>(g, t, src_buf, B, r, grid, l2_dist, s)
+               : launch_tb<BC_ADIABATIC, COLL_BGK>(g, t, src_buf, B, r, grid, l2_dist, s);
+  return cudaErrorNotSupported;
+}
+
+}  // namespace lbk

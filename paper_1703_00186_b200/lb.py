@@ -424,6 +424,14 @@ class Lattice:
         """Replay 2-step CUDA graphs in lb_step (needs a non-default stream)."""
         _check(lib().lb_set_option(self._ctx, 2, int(enable)))
 
+    def temporal(self, enable: bool = True, grid: int = 0, l2_prefetch: int = 0):
+        """Two steps per pass over HBM (LB_OPT_TEMPORAL; N = 1, walls, monitors off):
+        lb_step advances pairs of steps with the two-step kernel.  grid: CTAs
+        (0 = one per SM); l2_prefetch: L2 prefetch distance in columns (0 = off)."""
+        _check(lib().lb_set_option(self._ctx, 3, int(enable)))
+        _check(lib().lb_set_option(self._ctx, 4, int(grid)))
+        _check(lib().lb_set_option(self._ctx, 5, int(l2_prefetch)))
+
     def monitor(self, enable: bool = True):
         """Fused monitors: invariants reduced inside the step kernel (lb_monitor)."""
         _check(lib().lb_monitor(self._ctx, int(enable)))

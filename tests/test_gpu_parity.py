@@ -586,6 +586,60 @@ def test_tma_fused_step_bit_identical(lb, coll, bc, shape):
     assert np.array_equal(outs[0], outs[1])
 
 
+# ------------------------------------------------------------------ two steps per pass (temporal blocking)
+
+@pytest.mark.parametrize("coll", ["bgk", "regularized"])
+@pytest.mark.parametrize("bc", ["thermal", "adiabatic"])
+@pytest.mark.parametrize("shape", [(6, 6), (24, 40), (17, 131), (64, 32), (9, 300), (131, 200)])
+def test_two_step_kernel_bit_identical(lb, coll, bc, shape):
+    """LB_OPT_TEMPORAL (k_step2_tb: states n+1 and n+2 in one pass, n+1 kept in
+    shared memory) == two fused steps bit for bit: strips shorter than, equal
+    to and ragged against the 64-row strip height, a moved top strip, sweeps
+    that wrap periodically in x and CTA ranges that cross strip boundaries;
+    odd step counts end with one fused step."""
+    lx, ly = shape
+    st = oracle_state(lx, ly, seed=lx * 7 + ly)
+    outs = []
+    for tb in (False, True):
+        g = lb.Lattice(lx, ly, bc_y=bc, collision=coll, gravity=(1e-6, -1e-5))
+        if tb:
+            g.temporal(True)
+        g.set_state(st)
+        g.step(4)
+        g.step(3)
+        outs.append(g.gather())
+    assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("grid,l2", [(1, 0), (7, 4), (300, 8)])
+def test_two_step_kernel_grid_and_prefetch(lb, grid, l2):
+    """Any CTA count (one CTA sweeping everything, uneven ranges, more CTAs than
+    SMs) and any L2 prefetch distance give the same bits."""
+    lx, ly = 40, 150
+    st = oracle_state(lx, ly, seed=5)
+    ref = lb.Lattice(lx, ly)
+    ref.set_state(st)
+    ref.step(6)
+    g = lb.Lattice(lx, ly)
+    g.temporal(True, grid=grid, l2_prefetch=l2)
+    g.set_state(st)
+    g.step(6)
+    assert np.array_equal(g.gather(), ref.gather())
+
+
+def test_two_step_kernel_oracle_parity(lb):
+    """The two-step path against the oracle directly (RT state, 10 steps)."""
+    lx, ly = 64, 96
+    fields = lbgen.rt_macro(lx, ly, oracle.t0())
+    g, o = pair(lb, lx, ly)
+    g.temporal(True)
+    g.init_macro(*fields)
+    o.init_macro(*fields)
+    g.step(10)
+    o.step(10)
+    assert max_rel(g.gather(), o.get_state(0)) < TOL
+
+
 # ------------------------------------------------------------------ CUDA-graph stepping
 
 @pytest.mark.parametrize("coll,monitor", [("bgk", False), ("regularized", True)])

@@ -1,0 +1,60 @@
+"""Sweep of the two-step (temporal-blocking) kernel against the fused step.
+
+python tools/tb_bench.py [lx ly] — MLUPS of lb_step(K) at 1920x2048 (default)
+with LB_OPT_TEMPORAL off / on over a few CTA counts and L2 prefetch distances.
+CUDA events on the context stream, warm-up first; device-resident inputs
+(2 x 1.19 GB, far above L2).  Exploration tool, not the bench contract.
+"""
+import json
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__file__)))
+import lbgen  # noqa: E402
+import paper_1703_00186_b200 as lbm  # noqa: E402
+
+
+def run(lx, ly, tb, grid=0, l2=0, k=200, coll="bgk"):
+    s = torch.cuda.Stream()
+    g = lbm.Lattice(lx, ly, collision=coll, stream=s)
+    if tb:
+        g.temporal(True, grid=grid, l2_prefetch=l2)
+    g.init_macro(*lbgen.rt_macro(lx, ly, 1.0 / 1.19697977039307435897239 ** 2))
+    g.step(20)
+    g.sync()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(s):
+        e0.record(s)
+        g.step(k)
+        e1.record(s)
+    e1.synchronize()
+    ms = e0.elapsed_time(e1) / k
+    out = g.gather()
+    g.close()
+    return ms, lx * ly / ms / 1e3, out
+
+
+def main():
+    lx, ly = (int(sys.argv[1]), int(sys.argv[2])) if len(sys.argv) > 2 else (1920, 2048)
+    res = []
+    ms, ml, ref = run(lx, ly, False)
+    res.append({"tb": 0, "ms_per_step": ms, "mlups": ml})
+    print(json.dumps(res[-1]), flush=True)
+    for grid in (0, 296):
+        for l2 in (0, 2, 4, 8):
+            ms, ml, out = run(lx, ly, True, grid, l2)
+            res.append({"tb": 1, "grid": grid, "l2": l2, "ms_per_step": ms, "mlups": ml,
+                        "bit_identical": bool(np.array_equal(out, ref))})
+            print(json.dumps(res[-1]), flush=True)
+    for coll in ("regularized",):
+        ms, ml, ref = run(lx, ly, False, coll=coll)
+        print(json.dumps({"tb": 0, "coll": coll, "mlups": ml}), flush=True)
+        ms, ml, out = run(lx, ly, True, coll=coll)
+        print(json.dumps({"tb": 1, "coll": coll, "mlups": ml, "bit_identical": bool(np.array_equal(out, ref))}),
+              flush=True)
+
+
+if __name__ == "__main__":
+    main()
