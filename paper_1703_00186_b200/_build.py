@@ -50,23 +50,39 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return SO
     nd = nccl_dir()
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, ARCH, "-O3", "-lineinfo", "-std=c++17", "--fmad=false", "--expt-relaxed-constexpr",
-           "-Xcompiler", "-fPIC,-ffp-contract=off,-fno-fast-math",
-           "-Xptxas", "-v,-warn-spills",
-           "-shared", "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nd, "include"),
-           *sources(),
-           "-L", os.path.join(nd, "lib"), "-l:libnccl.so.2",
-           "-Xlinker", "-rpath," + os.path.join(nd, "lib"),
-           "-o", SO + ".tmp"]
-    r = subprocess.run(cmd, capture_output=True, text=True)
+    flags = [ARCH, "-O3", "-lineinfo", "-std=c++17", "--fmad=false", "--expt-relaxed-constexpr",
+             "-Xcompiler", "-fPIC,-ffp-contract=off,-fno-fast-math",
+             "-Xptxas", "-v,-warn-spills",
+             "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nd, "include")]
+    objdir = os.path.join(HERE, "build_obj")
+    os.makedirs(objdir, exist_ok=True)
+    # one nvcc per translation unit, in parallel (lb_kernels.cu and lb_tb.cu
+    # each take minutes), then one link
+    procs, objs = [], []
+    for src in sources():
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        objs.append(obj)
+        cmd = [nvcc, *flags, "-c", src, "-o", obj]
+        procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
+    log_txt, failed = [], False
+    for cmd, pr in procs:
+        out, _ = pr.communicate()
+        log_txt.append(" ".join(cmd) + "\n" + out)
+        failed |= pr.returncode != 0
+    link = [nvcc, ARCH, "-shared", *objs, "-L", os.path.join(nd, "lib"), "-l:libnccl.so.2",
+            "-Xlinker", "-rpath," + os.path.join(nd, "lib"), "-o", SO + ".tmp"]
+    if not failed:
+        r = subprocess.run(link, capture_output=True, text=True)
+        log_txt.append(" ".join(link) + "\n" + r.stdout + r.stderr)
+        failed = r.returncode != 0
     log = os.path.join(HERE, "build.log")
     with open(log, "w") as fh:
-        fh.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
-    if r.returncode != 0:
-        sys.stderr.write(r.stdout + r.stderr)
+        fh.write("\n".join(log_txt))
+    if failed:
+        sys.stderr.write("\n".join(log_txt))
         raise RuntimeError("nvcc failed (see %s)" % log)
     if verbose:
-        sys.stderr.write(r.stderr)
+        sys.stderr.write("\n".join(log_txt))
     os.replace(SO + ".tmp", SO)
     return SO
 
