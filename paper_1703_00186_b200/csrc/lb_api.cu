@@ -785,7 +785,7 @@ static int graph_two_steps(lb_ctx* c) {
 // mode, monitors off.  Bit-identical to two fused steps.
 static bool tb_usable(const lb_ctx* c) {
   return c->tb_on && c->tb && c->nranks == 1 && !c->comm && !c->peers_on && c->p.mode == LB_MODE_FUSED &&
-         c->p.bc_y != LB_PERIODIC && !c->mon_on;
+         c->p.bc_y != LB_PERIODIC && !c->mon_on && lbk::tb_layout_ok(c->g.ly);
 }
 
 static int step_tb(lb_ctx* c) {

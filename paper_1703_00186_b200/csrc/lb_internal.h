@@ -86,6 +86,8 @@ struct TbMaps {
   CUtensorMap pf[2];    // L2 prefetch of a column window, box {HT + 16, 37, 1}
 };
 TbMaps* tb_create(const Geo& g, double* buf0, double* buf1);
+// false for the few heights with no valid strip layout (HT < ly < HT + 6)
+bool tb_layout_ok(int ly);
 void tb_destroy(TbMaps* t);
 // lb_tb.cu's own copies of the wall constants and the Gram inverse
 cudaError_t tb_upload_constants(const double* k_bottom, const double* k_top, const double* ginv, cudaStream_t s);

@@ -141,53 +141,95 @@ __device__ __forceinline__ int wrap_col(int j, int lx) {
   return H + x;
 }
 
+// Walls as data (reading G9 i): a pull source row sy < 0 of population l reads
+// population refl(l) at row -1 - sy, a source row sy >= ly reads refl(l) at
+// 2 ly - 1 - sy.  Both rings hold those mirrored values in their rows beyond
+// the wall ("virtual rows"), so the plain gather is exact for every row and all
+// warps run ONE code path per phase (no mirror variant: fewer instructions, a
+// smaller instruction footprint, and wall strips cost what interior strips cost).
+//
+// State-n ring: column k (just arrived) gets its virtual rows from its own real
+// rows; rows outside population l's window are skipped (not pulled here).
+template <int PF, int P0, int R0>
+__device__ __forceinline__ void s0_virtual_rows(double* s0, int k, int ya, int ly, bool bottom, bool top) {
+#pragma unroll
+  for (int l = 0; l < Q; ++l) {
+    const int c = CY(l);
+    if (c == 0) continue;
+    // pointers indexed by absolute row
+    double* d = s0 + (SLOTS0_BEFORE<PF>(l) + k % L0<PF>(l)) * P0 - ya - A0(l);
+    const double* m = s0 + (SLOTS0_BEFORE<PF>(REFL(l)) + k % L0<PF>(l)) * P0 - ya - A0(REFL(l));
+    if (c > 0 && bottom) {
+      const int wbeg = ya + A0(l);  // first row of the window
+#pragma unroll
+      for (int q = 1; q <= 3; ++q)
+        if (q <= c && -q >= wbeg) d[-q] = m[q - 1];  // row -q <- refl row q - 1
+    }
+    if (c < 0 && top) {
+      const int wend = ya + A0(l) + R0;  // first row past the window
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+        if (q < -c && ly + q < wend) d[ly + q] = m[ly - 1 - q];  // row ly + q <- refl row ly - 1 - q
+    }
+  }
+}
+
+// Strip layout.  Strip s covers rows [ya, ya + HT) (ya even: TMA box starts
+// are 16-byte aligned).  A strip whose phase-1 rows [ya - 3, ya + HT + 3) reach
+// a wall band (3 rows) must contain that wall, because the mirror sources of
+// the band rows lie only in the windows of a strip that does.  So: strips from
+// the bottom at s·HT; the top strip moved down to end on the wall; the strip
+// below it moved down (if needed) to end >= 6 rows below the wall.  Heights
+// HT < ly < HT + 6 admit no such layout (tb_layout_ok; lb_step then uses
+// the one-step kernel).
+LB_HD inline int strip_ya(int s, int nstrips, int ly, int HT) {
+  if (s == nstrips - 1) return ((ly - HT + 1) & ~1) > 0 ? ((ly - HT + 1) & ~1) : 0;
+  if (s == nstrips - 2) {
+    const int lim = (ly - 6 - HT) & ~1;
+    return s * HT < lim ? s * HT : lim;
+  }
+  return s * HT;
+}
+
 // Phase 1 site update: state n+1 at row y = ya - 3 + i from the state-n ring
-// (iteration t), result into the state-(n+1) ring.  MIRROR: rows within 3 of
-// a wall (the warp-uniform non-interior path).
-template <int BC, int COLL, int PF, int P0, int R1, bool MIRROR>
-__device__ __forceinline__ void phase1(const double* s0, double* s1, int t, int i, int y, int ya, int ly,
+// (iteration t), result into the state-(n+1) ring; the rows next to a wall
+// also write the state-(n+1) virtual rows their values mirror into.
+template <int COLL, int PF, int P0, int R1>
+__device__ __forceinline__ void phase1(const double* s0, double* s1, int t, int i, int y, int ly, bool thermal,
                                        const Relax& r) {
   double f[Q];
   const int io = opaque(i);  // not hoistable: no per-population address registers
 #pragma unroll
-  for (int l = 0; l < Q; ++l) {
-    // REFL(l) has the same cx, so the same ring slot index
-    const int slot = (t - 3 - CX(l)) % L0<PF>(l);
-    int off = SLOTS0_BEFORE<PF>(l) * P0 + io - 3 - CY(l) - A0(l);
-    if (MIRROR) {
-      const int sy = y - CY(l);
-      if (sy < 0) off = SLOTS0_BEFORE<PF>(REFL(l)) * P0 + (-1 - sy) - ya - A0(REFL(l));
-      else if (sy >= ly) off = SLOTS0_BEFORE<PF>(REFL(l)) * P0 + (2 * ly - 1 - sy) - ya - A0(REFL(l));
-    }
-    f[l] = s0[slot * P0 + off];
-  }
-  if (MIRROR && BC == BC_THERMAL && (y < 3 || y >= ly - 3)) thermal_wall(f, y < 3 ? 0 : 1);
+  for (int l = 0; l < Q; ++l)
+    f[l] = s0[((t - 3 - CX(l)) % L0<PF>(l)) * P0 + SLOTS0_BEFORE<PF>(l) * P0 + io - 3 - CY(l) - A0(l)];
+  const bool wall = y < 3 || y >= ly - 3;
+  if (thermal && wall) thermal_wall(f, y < 3 ? 0 : 1);
   if (COLL == COLL_REGULARIZED) collide_site_reg(f, r);
   else collide_site(f, r);
 #pragma unroll
   for (int l = 0; l < Q; ++l) s1[(SLOTS1_BEFORE(l) + (t % L1(l))) * R1 + io] = f[l];
+  if (wall) {
+    // virtual row of refl(l): -1 - y (bottom) or 2 ly - 1 - y (top); ring row
+    // index = absolute row - (ya - 3), and i = y - (ya - 3)
+    const int vi = y < 3 ? i - 2 * y - 1 : i + 2 * (ly - 1 - y) + 1;
+    if (vi >= 0 && vi < R1) {
+#pragma unroll
+      for (int l = 0; l < Q; ++l) s1[(SLOTS1_BEFORE(REFL(l)) + (t % L1(l))) * R1 + vi] = f[l];
+    }
+  }
 }
 
 // Phase 2 site update: state n+2 at row y = ya + i, column c2, from the
 // state-(n+1) ring, stored to B (+ B's halo for the 3+3 border columns).
-template <int BC, int COLL, int R1, bool MIRROR>
+template <int COLL, int R1>
 __device__ __forceinline__ void phase2(const double* s1, double* __restrict__ B, const Geo& g, int t, int i,
-                                       int y, int ya, int c2, const Relax& r) {
+                                       int y, int c2, bool thermal, const Relax& r) {
   const int ly = g.ly;
   double f[Q];
   const int io = opaque(i);
 #pragma unroll
-  for (int l = 0; l < Q; ++l) {
-    const int slot = (t - 4 - CX(l)) % L1(l);
-    int off = SLOTS1_BEFORE(l) * R1 + io + 3 - CY(l);
-    if (MIRROR) {
-      const int sy = y - CY(l);
-      if (sy < 0) off = SLOTS1_BEFORE(REFL(l)) * R1 + (-1 - sy) - ya + 3;
-      else if (sy >= ly) off = SLOTS1_BEFORE(REFL(l)) * R1 + (2 * ly - 1 - sy) - ya + 3;
-    }
-    f[l] = s1[slot * R1 + off];
-  }
-  if (MIRROR && BC == BC_THERMAL && (y < 3 || y >= ly - 3)) thermal_wall(f, y < 3 ? 0 : 1);
+  for (int l = 0; l < Q; ++l) f[l] = s1[((t - 4 - CX(l)) % L1(l)) * R1 + SLOTS1_BEFORE(l) * R1 + io + 3 - CY(l)];
+  if (thermal && (y < 3 || y >= ly - 3)) thermal_wall(f, y < 3 ? 0 : 1);
   if (COLL == COLL_REGULARIZED) collide_site_reg(f, r);
   else collide_site(f, r);
   const int nyp = opaque(g.nyp);
@@ -210,10 +252,10 @@ __device__ __forceinline__ void phase2(const double* s1, double* __restrict__ B,
 // Warps [0, NW1): phase 1; [NW1, NW1 + NW2): phase 2; the last warp is the
 // TMA producer (its lane 0 issues the 37 window loads of a column while the
 // compute warps work, so the issue cost is off their critical path).
-template <int BC, int COLL, int HT, int PF>
+template <int COLL, int HT, int PF>
 __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
     k_step2_tb(const __grid_constant__ CUtensorMap src, const __grid_constant__ CUtensorMap pf_map,
-               double* __restrict__ B, Geo g, Relax r, int nstrips, int l2_dist) {
+               double* __restrict__ B, Geo g, Relax r, int nstrips, int l2_dist, int thermal) {
   using C = TbCfg<HT, PF>;
   constexpr int R0 = C::R0, P0 = C::P0, R1 = C::R1, NB = C::NB;
   extern __shared__ __align__(128) double sm[];
@@ -242,13 +284,16 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
     const int x1 = (int)std::min<int64_t>(lx, x0 + (u_end - u));
     u += x1 - x0;
     const int xs = H + x0, W = x1 - x0;  // output columns [xs, xs + W)
-    // strip rows [ya, ya + HT); the top strip is moved down to end on the wall,
-    // ya kept even (TMA box starts must be 16-byte aligned): it may then
-    // reach one row past the wall, which is simply not computed
-    const int ya = std::max(0, std::min(strip * HT, (ly - HT + 1) & ~1));
+    // strip rows [ya, ya + HT) (strip_ya); the top strip may reach one row
+    // past the wall, which is simply not computed
+    const int ya = strip_ya(strip, nstrips, ly, HT);
     const int ncols = W + 12;         // state-n columns of this sweep
     const int niter = W + 13;         // iterations
     const int rbase = g.y0 + ya;      // internal row of ya
+    // phase-1 warp rows [ya - 3 + 32 w, +32): does it pull across a wall?
+    const int wr0 = ya - 3 + 32 * warp, wr1 = std::min(wr0 + 32, ya + HT + 3);
+    const bool vbottom = warp < C::NW1 && wr0 < 3 && wr1 > 0;
+    const bool vtop = warp < C::NW1 && wr1 > ly - 3 && wr0 < ly;
 
     auto issue = [&](int k) {         // TMA of sweep column k (producer only)
       const uint32_t kb = kglob + (uint32_t)k;
@@ -285,29 +330,24 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
       if (t < ncols) {
         const uint32_t kb = kglob + (uint32_t)t;
         mbar_wait(smem_u32(bars + kb % NB), (kb / NB) & 1);
+        // the warps that pull across a wall fill column t's virtual rows
+        // themselves (redundantly if two do: same values) before reading it
+        if (vbottom || vtop) {
+          if ((tid & 31) == 0) s0_virtual_rows<PF, P0, R0>(s0, t, ya, ly, vbottom, vtop);
+          __syncwarp();
+        }
       }
       if (warp < C::NW1) {
         // phase 1: state n+1 at column c1 = xs - 9 + t, rows [ya-3, ya+HT+3)
         const int i = tid;
         const int y = ya - 3 + i;
-        if (t >= 6 && t < W + 12 && i < R1 && y >= 0 && y < ly) {
-          const int wy0 = ya - 3 + (tid & ~31);
-          if (wy0 >= 3 && wy0 + 32 <= ly - 3)
-            phase1<BC, COLL, PF, P0, R1, false>(s0, s1, t, i, y, ya, ly, r);
-          else
-            phase1<BC, COLL, PF, P0, R1, true>(s0, s1, t, i, y, ya, ly, r);
-        }
+        if (t >= 6 && t < W + 12 && i < R1 && y >= 0 && y < ly)
+          phase1<COLL, PF, P0, R1>(s0, s1, t, i, y, ly, thermal, r);
       } else {
         // phase 2: state n+2 at column c2 = xs - 13 + t, rows [ya, ya+HT)
         const int i = tid - 32 * C::NW1;
         const int y = ya + i;
-        if (t >= 13 && i < HT && y < ly) {
-          const int wy0 = ya + (i & ~31);
-          if (wy0 >= 3 && wy0 + 32 <= ly - 3)
-            phase2<BC, COLL, R1, false>(s1, B, g, t, i, y, ya, xs - 13 + t, r);
-          else
-            phase2<BC, COLL, R1, true>(s1, B, g, t, i, y, ya, xs - 13 + t, r);
-        }
+        if (t >= 13 && i < HT && y < ly) phase2<COLL, R1>(s1, B, g, t, i, y, xs - 13 + t, thermal, r);
       }
     }
     kglob += (uint32_t)ncols;
@@ -336,14 +376,14 @@ bool encode(CUtensorMap* m, double* base, const Geo& g, int box_rows, int box_po
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-constexpr int TB_HT = 56;
-constexpr int TB_PF = 3;
+constexpr int TB_HT = 70;
+constexpr int TB_PF = 1;
 using Cfg = TbCfg<TB_HT, TB_PF>;
 
-template <int BC, int COLL>
+template <int COLL>
 cudaError_t launch_tb(const Geo& g, const TbMaps* t, int src_buf, double* B, const Relax& r, int grid,
-                      int l2_dist, cudaStream_t s) {
-  auto kern = k_step2_tb<BC, COLL, TB_HT, TB_PF>;
+                      int l2_dist, int thermal, cudaStream_t s) {
+  auto kern = k_step2_tb<COLL, TB_HT, TB_PF>;
   static unsigned long long done_mask = 0;  // opt-in smem is a per-device attribute
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -356,11 +396,13 @@ cudaError_t launch_tb(const Geo& g, const TbMaps* t, int src_buf, double* B, con
   const int nstrips = (g.ly + TB_HT - 1) / TB_HT;
   const int64_t U = (int64_t)nstrips * g.lx;
   const int G = (int)std::min<int64_t>(grid, U);
-  kern<<<G, Cfg::NT, Cfg::SMEM, s>>>(t->load[src_buf], t->pf[src_buf], B, g, r, nstrips, l2_dist);
+  kern<<<G, Cfg::NT, Cfg::SMEM, s>>>(t->load[src_buf], t->pf[src_buf], B, g, r, nstrips, l2_dist, thermal);
   return cudaGetLastError();
 }
 
 }  // namespace
+
+bool tb_layout_ok(int ly) { return ly <= TB_HT || ly >= TB_HT + 6; }
 
 TbMaps* tb_create(const Geo& g, double* buf0, double* buf1) {
   if (g.y0 % 2 || g.nyp % 2 || g.lx < 2 * H) return nullptr;
@@ -388,14 +430,10 @@ cudaError_t tb_upload_constants(const double* k_bottom, const double* k_top, con
 
 cudaError_t launch_step2_tb(const Geo& g, const TbMaps* t, int src_buf, double* B, int bc, int coll,
                             const Relax& r, int grid, int l2_dist, cudaStream_t s) {
-  if (bc == BC_THERMAL)
-    return coll == COLL_REGULARIZED ? launch_tb<BC_THERMAL, COLL_REGULARIZED>(g, t, src_buf, B, r, grid, l2_dist, s)
-                                    : launch_tb<BC_THERMAL, COLL_BGK>(g, t, src_buf, B, r, grid, l2_dist, s);
-  if (bc == BC_ADIABATIC)
-    return coll == COLL_REGULARIZED
-               ? launch_tb<BC_ADIABATIC, COLL_REGULARIZED>(g, t, src_buf, B, r, grid, l2_dist, s)
-               : launch_tb<BC_ADIABATIC, COLL_BGK>(g, t, src_buf, B, r, grid, l2_dist, s);
-  return cudaErrorNotSupported;
+  if (bc != BC_THERMAL && bc != BC_ADIABATIC) return cudaErrorNotSupported;
+  const int thermal = bc == BC_THERMAL;
+  return coll == COLL_REGULARIZED ? launch_tb<COLL_REGULARIZED>(g, t, src_buf, B, r, grid, l2_dist, thermal, s)
+                                  : launch_tb<COLL_BGK>(g, t, src_buf, B, r, grid, l2_dist, thermal, s);
 }
 
 }  // namespace lbk

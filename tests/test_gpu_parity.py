@@ -590,7 +590,8 @@ def test_tma_fused_step_bit_identical(lb, coll, bc, shape):
 
 @pytest.mark.parametrize("coll", ["bgk", "regularized"])
 @pytest.mark.parametrize("bc", ["thermal", "adiabatic"])
-@pytest.mark.parametrize("shape", [(6, 6), (24, 40), (17, 131), (64, 32), (9, 300), (131, 200)])
+@pytest.mark.parametrize("shape", [(6, 6), (24, 40), (17, 131), (64, 32), (9, 300), (131, 200), (12, 60), (10, 75),
+                                   (8, 146), (7, 147), (11, 72), (9, 76), (13, 145), (9, 211)])
 def test_two_step_kernel_bit_identical(lb, coll, bc, shape):
     """LB_OPT_TEMPORAL (k_step2_tb: states n+1 and n+2 in one pass, n+1 kept in
     shared memory) == two fused steps bit for bit: strips shorter than, equal

@@ -6,6 +6,7 @@ CUDA events on the context stream, warm-up first; device-resident inputs
 (2 x 1.19 GB, far above L2).  Exploration tool, not the bench contract.
 """
 import json
+import os
 import sys
 
 import numpy as np
@@ -42,8 +43,10 @@ def main():
     ms, ml, ref = run(lx, ly, False)
     res.append({"tb": 0, "ms_per_step": ms, "mlups": ml})
     print(json.dumps(res[-1]), flush=True)
-    for grid in (0, 296):
-        for l2 in (0, 2, 4, 8):
+    grids = [int(x) for x in os.environ.get("TB_GRIDS", "0,296").split(",")]
+    l2s = [int(x) for x in os.environ.get("TB_L2", "0,2,4,8").split(",")]
+    for grid in grids:
+        for l2 in l2s:
             ms, ml, out = run(lx, ly, True, grid, l2)
             res.append({"tb": 1, "grid": grid, "l2": l2, "ms_per_step": ms, "mlups": ml,
                         "bit_identical": bool(np.array_equal(out, ref))})
