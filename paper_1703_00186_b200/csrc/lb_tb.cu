@@ -1,5 +1,5 @@
 // lb_tb.cu — two time steps per pass over HBM (temporal blocking of the fused
-// pull step, §8a5 extended; DESIGN.md §6 "k_step2_tb").
+// pull step, §8a5 extended; DESIGN.md §8 "k_step2_tb").
 //
 // The fused step (k_step_fused) moves 592 B/site per step and runs at the HBM
 // copy roof, with the FP64 pipe ~25 % busy.  This kernel computes steps n+1 AND
@@ -10,38 +10,36 @@
 // result is bit-identical to two k_step_fused launches.
 //
 // Tiling.  A CTA owns a strip of HT rows [ya, ya+HT) and sweeps a range of
-// output columns [xs, xe) in x.  Iteration t of a sweep:
-//   * TMA (one elected thread) loads state-n column k = t + PF (sweep index;
-//     global column xs - 6 + k, wrapped periodically — N = 1 needs no halo):
-//     for every population l the rows [ya - 3 - cy_l, ya + HT + 3 - cy_l) it
-//     will be pulled from, rounded out to a 16-byte box start (the TMA
-//     alignment rule, tools/tma_probe.cu) — R0 = HT + 8 rows;
-//   * phase 1 (warps [0, NW1)): step n+1 at column c1 = xs - 9 + t for the
+// output columns [xs, xs + W) in x.  Iteration t of a sweep:
+//   * TMA: for every population l, the window of state n that phase 1 of
+//     iteration t + PF pulls it from — column c1(t + PF) - cx_l (wrapped
+//     periodically: N = 1 needs no halo), rows [ya - 3 - cy_l, ya + HT + 3 -
+//     cy_l) rounded out to a 16-byte box start (the TMA alignment rule,
+//     tools/tma_probe.cu), R0 = HT + 8 rows.  The TMA coordinates perform the
+//     whole pull (propagate), so the state-n ring is just PF + 1 buffers per
+//     population.  The 37 loads are issued by the lane 0s of all warps;
+//   * phase 1 (warps [0, NW1)): state n+1 at column c1 = xs - 3 + t for the
 //     R1 = HT + 6 rows [ya - 3, ya + HT + 3) (the ±3-row apron step n+2 pulls
-//     from), gathered from the state-n ring, written to the state-(n+1) ring;
-//   * phase 2 (warps [NW1, NW1+NW2)): step n+2 at column c2 = xs - 13 + t for
-//     the HT rows of the strip, gathered from the state-(n+1) ring, stored to B
+//     from), written to the state-(n+1) ring;
+//   * phase 2 (warps [NW1, NW1 + NW2)): state n+2 at column c2 = c1 - 4 for the
+//     HT rows of the strip, gathered from the state-(n+1) ring, stored to B
 //     (and, for the 3+3 border columns, into B's halo: the next step's wrap).
-// Both phases of an iteration are independent (phase 2 lags by one extra
-// column), so ONE __syncthreads per iteration orders everything.
+// Both phases of an iteration are independent (phase 2 lags by one column more
+// than the ±3 reach), so ONE __syncthreads per iteration orders everything.
 //
-// Rings.  Population l of a column is pulled by the output column x + cx_l, so
-// it lives cx_l + 3 iterations after arrival: the state-n ring of population l
-// has L0 = cx_l + 4 + PF slots (PF = TMA prefetch depth), the state-(n+1) ring
-// L1 = cx_l + 5.  Summed over the 37 populations that is 37·(4+PF) and 37·5
-// column slots instead of 7 + 7 full columns.  State-n slots are padded to
-// 128 bytes (TMA destination alignment).  HT = 56, PF = 3: 224 KB smem.
+// State-(n+1) ring.  Population l of column c1 is pulled by phase 2 at column
+// c1 + cx_l, cx_l + 4 iterations later: cx_l + 5 slots of R1 rows (185 slots
+// over the 37 populations).  HT = 104, PF = 1: 66 KB (state n) + 163 KB
+// (state n+1) of shared memory, 214 sites per iteration, 8 warps.
 //
-// Walls (G9): the strips next to a wall pull mirrored populations (REFL(l) at
-// the image row) from the same rings — every image row lies inside the window
-// loaded for REFL(l); warps whose rows are all >= 3 rows from both walls take
-// the mirror-free path (warp-uniform).  Periodic-Y geometry is not supported
-// here (the 1-step kernel serves it).
+// Walls (G9) are data: the mirrored populations are copied into ring rows
+// beyond each wall ("virtual rows"), so the plain gather is exact for every row
+// and all warps run ONE code path per phase.  Periodic-Y geometry is not
+// supported here (the 1-step kernel serves it).
 //
 // Work split: the strips × lx column-units are cut into gridDim.x contiguous
 // ranges (one CTA per SM, persistent); a range crossing a strip boundary is two
-// sweeps.  A strip that would pass the top wall is moved down to end on it
-// (rows computed twice produce identical values).
+// sweeps (strip_ya: the layout).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -61,8 +59,6 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)_
 // y0 are even)
 LB_HD constexpr int A0(int l) { return -3 - CY(l) - ((CY(l) + 1) & 1); }
 
-template <int PF>
-LB_HD constexpr int L0(int l) { return CX(l) + 4 + PF; }
 LB_HD constexpr int L1(int l) { return CX(l) + 5; }
 
 // Literal tables (a constexpr loop evaluated in device code is NOT folded by
@@ -89,27 +85,37 @@ constexpr bool tables_ok() {
 }
 static_assert(tables_ok(), "CXSUM / REFL tables");
 
-// ring slots of the populations before l (state n, state n+1)
-template <int PF>
-LB_HD constexpr int SLOTS0_BEFORE(int l) { return CXSUM(l) + (4 + PF) * l; }
+// state-(n+1) ring slots of the populations before l
 LB_HD constexpr int SLOTS1_BEFORE(int l) { return CXSUM(l) + 5 * l; }
+
+// per-population TMA parameters for the issuing threads: (cx_l, A0(l))
+__constant__ int2 c_tb_pop[Q] = {
+#define LBTB_P(l) {CX(l), A0(l)}
+    LBTB_P(0),  LBTB_P(1),  LBTB_P(2),  LBTB_P(3),  LBTB_P(4),  LBTB_P(5),  LBTB_P(6),  LBTB_P(7),
+    LBTB_P(8),  LBTB_P(9),  LBTB_P(10), LBTB_P(11), LBTB_P(12), LBTB_P(13), LBTB_P(14), LBTB_P(15),
+    LBTB_P(16), LBTB_P(17), LBTB_P(18), LBTB_P(19), LBTB_P(20), LBTB_P(21), LBTB_P(22), LBTB_P(23),
+    LBTB_P(24), LBTB_P(25), LBTB_P(26), LBTB_P(27), LBTB_P(28), LBTB_P(29), LBTB_P(30), LBTB_P(31),
+    LBTB_P(32), LBTB_P(33), LBTB_P(34), LBTB_P(35), LBTB_P(36)};
+#undef LBTB_P
 
 template <int HT_, int PF_>
 struct TbCfg {
   static constexpr int HT = HT_;
   static constexpr int PF = PF_;
   static constexpr int R0 = HT + 8;                 // TMA box rows of a state-n window
-  static constexpr int P0 = (R0 + 15) / 16 * 16;    // slot pitch: TMA smem destinations are 128-byte aligned
+  static constexpr int P0 = (R0 + 15) / 16 * 16;    // buffer pitch: TMA smem destinations are 128-byte aligned
   static constexpr int R1 = HT + 6;
-  static constexpr int NW1 = (R1 + 31) / 32;
-  static constexpr int NW2 = (HT + 31) / 32;
-  static constexpr int NT = 32 * (NW1 + NW2 + 1);  // + the TMA producer warp
-  static constexpr int NB = PF + 1;  // mbarriers (columns in flight + the one being consumed)
-  static constexpr int S0_DBL = SLOTS0_BEFORE<PF>(Q) * P0;
+  static constexpr int NW1 = (R1 + 31) / 32;        // phase-1 warps
+  static constexpr int NW2 = (HT + 31) / 32;        // phase-2 warps
+  static constexpr int NW = NW1 + NW2;
+  static constexpr int NT = 32 * NW;
+  static constexpr int NB = PF + 1;                 // state-n buffers per population = mbarriers
+  static constexpr int S0_DBL = Q * NB * P0;
   static constexpr int S1_DBL = SLOTS1_BEFORE(Q) * R1;
   static constexpr size_t SMEM = (size_t)(S0_DBL + S1_DBL) * sizeof(double) + NB * sizeof(uint64_t);
   static_assert(R0 % 2 == 0 && R0 <= 256, "TMA box rows");
   static_assert(SMEM <= 232448, "shared memory per CTA");
+  static_assert(NW <= 8, "two warps per scheduler at most (64 KB register file per scheduler)");
 };
 
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
@@ -148,32 +154,6 @@ __device__ __forceinline__ int wrap_col(int j, int lx) {
 // warps run ONE code path per phase (no mirror variant: fewer instructions, a
 // smaller instruction footprint, and wall strips cost what interior strips cost).
 //
-// State-n ring: column k (just arrived) gets its virtual rows from its own real
-// rows; rows outside population l's window are skipped (not pulled here).
-template <int PF, int P0, int R0>
-__device__ __forceinline__ void s0_virtual_rows(double* s0, int k, int ya, int ly, bool bottom, bool top) {
-#pragma unroll
-  for (int l = 0; l < Q; ++l) {
-    const int c = CY(l);
-    if (c == 0) continue;
-    // pointers indexed by absolute row
-    double* d = s0 + (SLOTS0_BEFORE<PF>(l) + k % L0<PF>(l)) * P0 - ya - A0(l);
-    const double* m = s0 + (SLOTS0_BEFORE<PF>(REFL(l)) + k % L0<PF>(l)) * P0 - ya - A0(REFL(l));
-    if (c > 0 && bottom) {
-      const int wbeg = ya + A0(l);  // first row of the window
-#pragma unroll
-      for (int q = 1; q <= 3; ++q)
-        if (q <= c && -q >= wbeg) d[-q] = m[q - 1];  // row -q <- refl row q - 1
-    }
-    if (c < 0 && top) {
-      const int wend = ya + A0(l) + R0;  // first row past the window
-#pragma unroll
-      for (int q = 0; q < 3; ++q)
-        if (q < -c && ly + q < wend) d[ly + q] = m[ly - 1 - q];  // row ly + q <- refl row ly - 1 - q
-    }
-  }
-}
-
 // Strip layout.  Strip s covers rows [ya, ya + HT) (ya even: TMA box starts
 // are 16-byte aligned).  A strip whose phase-1 rows [ya - 3, ya + HT + 3) reach
 // a wall band (3 rows) must contain that wall, because the mirror sources of
@@ -191,17 +171,44 @@ LB_HD inline int strip_ya(int s, int nstrips, int ly, int HT) {
   return s * HT;
 }
 
-// Phase 1 site update: state n+1 at row y = ya - 3 + i from the state-n ring
-// (iteration t), result into the state-(n+1) ring; the rows next to a wall
-// also write the state-(n+1) virtual rows their values mirror into.
-template <int COLL, int PF, int P0, int R1>
-__device__ __forceinline__ void phase1(const double* s0, double* s1, int t, int i, int y, int ly, bool thermal,
-                                       const Relax& r) {
+// State-n buffer b (just arrived): population l's window comes from the same
+// column as refl(l)'s (same cx), so the virtual rows are copies within buffer
+// b; rows outside population l's window are skipped (not pulled here).
+template <int NB, int P0, int R0>
+__device__ __forceinline__ void s0_virtual_rows(double* s0, int b, int ya, int ly, bool bottom, bool top) {
+#pragma unroll
+  for (int l = 0; l < Q; ++l) {
+    const int c = CY(l);
+    if (c == 0) continue;
+    // pointers indexed by absolute row
+    double* d = s0 + (l * NB + b) * P0 - ya - A0(l);
+    const double* m = s0 + (REFL(l) * NB + b) * P0 - ya - A0(REFL(l));
+    if (c > 0 && bottom) {
+      const int wbeg = ya + A0(l);  // first row of the window
+#pragma unroll
+      for (int q = 1; q <= 3; ++q)
+        if (q <= c && -q >= wbeg) d[-q] = m[q - 1];  // row -q <- refl row q - 1
+    }
+    if (c < 0 && top) {
+      const int wend = ya + A0(l) + R0;  // first row past the window
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+        if (q < -c && ly + q < wend) d[ly + q] = m[ly - 1 - q];  // row ly + q <- refl row ly - 1 - q
+    }
+  }
+}
+
+// Phase 1 site update: state n+1 at row y = ya - 3 + i from state-n buffer b
+// (the pulled values), result into the state-(n+1) ring slot of iteration t;
+// the rows next to a wall also write the virtual rows their values mirror into.
+template <int COLL, int NB, int P0, int R1>
+__device__ __forceinline__ void phase1(const double* s0, double* s1, int b, int t, int i, int y, int ly,
+                                       bool thermal, const Relax& r) {
   double f[Q];
   const int io = opaque(i);  // not hoistable: no per-population address registers
+  const double* sb = s0 + b * P0 + io;
 #pragma unroll
-  for (int l = 0; l < Q; ++l)
-    f[l] = s0[((t - 3 - CX(l)) % L0<PF>(l)) * P0 + SLOTS0_BEFORE<PF>(l) * P0 + io - 3 - CY(l) - A0(l)];
+  for (int l = 0; l < Q; ++l) f[l] = sb[l * NB * P0 - 3 - CY(l) - A0(l)];
   const bool wall = y < 3 || y >= ly - 3;
   if (thermal && wall) thermal_wall(f, y < 3 ? 0 : 1);
   if (COLL == COLL_REGULARIZED) collide_site_reg(f, r);
@@ -249,9 +256,7 @@ __device__ __forceinline__ void phase2(const double* s1, double* __restrict__ B,
   }
 }
 
-// Warps [0, NW1): phase 1; [NW1, NW1 + NW2): phase 2; the last warp is the
-// TMA producer (its lane 0 issues the 37 window loads of a column while the
-// compute warps work, so the issue cost is off their critical path).
+// Warps [0, NW1): phase 1; [NW1, NW1 + NW2): phase 2.
 template <int COLL, int HT, int PF>
 __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
     k_step2_tb(const __grid_constant__ CUtensorMap src, const __grid_constant__ CUtensorMap pf_map,
@@ -265,9 +270,8 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
   const int lx = g.lx, ly = g.ly;
-  const bool producer = tid == 32 * (C::NW1 + C::NW2);
 
-  if (producer) {
+  if (tid == 0) {
     for (int i = 0; i < NB; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bars + i)));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -276,7 +280,7 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
   const int64_t U = (int64_t)nstrips * lx;
   int64_t u = U * blockIdx.x / gridDim.x;
   const int64_t u_end = U * (blockIdx.x + 1) / gridDim.x;
-  uint32_t kglob = 0;  // columns loaded by this CTA over all its sweeps (barrier phase)
+  uint32_t kglob = 0;  // load iterations of this CTA over all its sweeps (barrier phase)
 
   while (u < u_end) {
     const int strip = (int)(u / lx);
@@ -287,70 +291,78 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
     // strip rows [ya, ya + HT) (strip_ya); the top strip may reach one row
     // past the wall, which is simply not computed
     const int ya = strip_ya(strip, nstrips, ly, HT);
-    const int ncols = W + 12;         // state-n columns of this sweep
-    const int niter = W + 13;         // iterations
+    const int nload = W + 6;          // phase-1 iterations (columns c1 = xs - 3 + t)
+    const int niter = W + 7;          // + the phase-2 lag
     const int rbase = g.y0 + ya;      // internal row of ya
     // phase-1 warp rows [ya - 3 + 32 w, +32): does it pull across a wall?
     const int wr0 = ya - 3 + 32 * warp, wr1 = std::min(wr0 + 32, ya + HT + 3);
     const bool vbottom = warp < C::NW1 && wr0 < 3 && wr1 > 0;
     const bool vtop = warp < C::NW1 && wr1 > ly - 3 && wr0 < ly;
 
-    auto issue = [&](int k) {         // TMA of sweep column k (producer only)
+    // TMA of the state-n window of population l that phase 1 of iteration k
+    // pulls (column c1(k) - cx_l, rows from ya + A0(l)); one thread per
+    // population; the thread of l = 0 also posts the expected bytes
+    // (complete_tx may precede it: the phase cannot complete before that
+    // single arrival)
+    auto issue_one = [&](int k, int l) {
       const uint32_t kb = kglob + (uint32_t)k;
       const uint32_t bar = smem_u32(bars + kb % NB);
-      const int col = wrap_col(xs - 6 + k, lx);
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
-                   "r"((uint32_t)(Q * R0 * sizeof(double))));
-#pragma unroll
-      for (int l = 0; l < Q; ++l) {
-        double* dst = s0 + (SLOTS0_BEFORE<PF>(l) + (k % L0<PF>(l))) * P0;
-        asm volatile(
-            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
-            " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
-            "l"(&src), "r"(rbase + A0(l)), "r"(l), "r"(col), "r"(bar)
-            : "memory");
-      }
-      if (l2_dist > 0 && k + l2_dist < ncols) {
-        const int pcol = wrap_col(xs - 6 + k + l2_dist, lx);
-        asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(&pf_map),
-                     "r"(rbase - 8), "r"(0), "r"(pcol)
-                     : "memory");
-      }
-    };
-
-    if (producer)
-      for (int k = 0; k < PF && k < ncols; ++k) issue(k);
-
-    for (int t = 0; t < niter; ++t) {
-      __syncthreads();  // every read of iteration t-1 is done: the slots refilled below are free
-      if (warp == C::NW1 + C::NW2) {
-        if (producer && t + PF < ncols) issue(t + PF);
-        continue;
-      }
-      if (t < ncols) {
-        const uint32_t kb = kglob + (uint32_t)t;
-        mbar_wait(smem_u32(bars + kb % NB), (kb / NB) & 1);
-        // the warps that pull across a wall fill column t's virtual rows
-        // themselves (redundantly if two do: same values) before reading it
-        if (vbottom || vtop) {
-          if ((tid & 31) == 0) s0_virtual_rows<PF, P0, R0>(s0, t, ya, ly, vbottom, vtop);
-          __syncwarp();
+      const int buf = (int)(kb % NB);
+      const int c1 = xs - 3 + k;
+      if (l == 0) {
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                     "r"((uint32_t)(Q * R0 * sizeof(double))));
+        if (l2_dist > 0 && k + l2_dist < nload) {
+          // the newest column any population of iteration k + l2_dist touches
+          const int pcol = wrap_col(c1 + l2_dist + 3, lx);
+          asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(&pf_map),
+                       "r"(rbase - 8), "r"(0), "r"(pcol)
+                       : "memory");
         }
       }
+      const int2 pc = c_tb_pop[l];  // (cx_l, A0(l))
+      const double* dst = s0 + (l * NB + buf) * P0;
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+          " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+          "l"(&src), "r"(rbase + pc.y), "r"(l), "r"(wrap_col(c1 - pc.x, lx)), "r"(bar)
+          : "memory");
+    };
+    // lanes [0, 5) of warp w issue populations 5 w + lane (8 warps cover 37)
+    const int my_pop = 5 * warp + (tid & 31);
+    const bool issuer = (tid & 31) < 5 && my_pop < Q;
+    static_assert(5 * C::NW >= Q, "not enough issuing lanes");
+
+    if (issuer)
+      for (int k = 0; k < PF && k < nload; ++k) issue_one(k, my_pop);
+
+    for (int t = 0; t < niter; ++t) {
+      __syncthreads();  // every read of iteration t-1 is done: the buffers refilled below are free
+      if (issuer && t + PF < nload) issue_one(t + PF, my_pop);
       if (warp < C::NW1) {
-        // phase 1: state n+1 at column c1 = xs - 9 + t, rows [ya-3, ya+HT+3)
-        const int i = tid;
-        const int y = ya - 3 + i;
-        if (t >= 6 && t < W + 12 && i < R1 && y >= 0 && y < ly)
-          phase1<COLL, PF, P0, R1>(s0, s1, t, i, y, ly, thermal, r);
-      } else {
-        // phase 2: state n+2 at column c2 = xs - 13 + t, rows [ya, ya+HT)
+        if (t < nload) {
+          // phase 1: state n+1 at column c1 = xs - 3 + t, rows [ya-3, ya+HT+3)
+          const uint32_t kb = kglob + (uint32_t)t;
+          const int buf = (int)(kb % NB);
+          mbar_wait(smem_u32(bars + buf), (kb / NB) & 1);
+          // the warps that pull across a wall fill the virtual rows themselves
+          // (redundantly if two do: same values) before reading them
+          if (vbottom || vtop) {
+            if ((tid & 31) == 0) s0_virtual_rows<NB, P0, R0>(s0, buf, ya, ly, vbottom, vtop);
+            __syncwarp();
+          }
+          const int i = tid;
+          const int y = ya - 3 + i;
+          if (i < R1 && y >= 0 && y < ly) phase1<COLL, NB, P0, R1>(s0, s1, buf, t, i, y, ly, thermal, r);
+        }
+      } else if (t >= 7) {
+        // phase 2: state n+2 at column c2 = xs - 7 + t, rows [ya, ya+HT)
         const int i = tid - 32 * C::NW1;
         const int y = ya + i;
-        if (t >= 13 && i < HT && y < ly) phase2<COLL, R1>(s1, B, g, t, i, y, xs - 13 + t, thermal, r);
+        if (i < HT && y < ly) phase2<COLL, R1>(s1, B, g, t, i, y, xs - 7 + t, thermal, r);
       }
     }
-    kglob += (uint32_t)ncols;
+    kglob += (uint32_t)nload;
     __syncthreads();  // the next sweep refills every ring
   }
 }
@@ -376,7 +388,7 @@ bool encode(CUtensorMap* m, double* base, const Geo& g, int box_rows, int box_po
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-constexpr int TB_HT = 70;
+constexpr int TB_HT = 104;
 constexpr int TB_PF = 1;
 using Cfg = TbCfg<TB_HT, TB_PF>;
 
