@@ -171,31 +171,37 @@ LB_HD inline int strip_ya(int s, int nstrips, int ly, int HT) {
   return s * HT;
 }
 
-// State-n buffer b (just arrived): population l's window comes from the same
-// column as refl(l)'s (same cx), so the virtual rows are copies within buffer
-// b; rows outside population l's window are skipped (not pulled here).
-template <int NB, int P0, int R0>
-__device__ __forceinline__ void s0_virtual_rows(double* s0, int b, int ya, int ly, bool bottom, bool top) {
-#pragma unroll
+// State-n virtual rows.  Buffer b (just arrived): population l's window comes
+// from the same column as refl(l)'s (same cx), so the virtual rows are copies
+// within buffer b — 26 per wall (cy_l > 0: rows -1..-cy_l at the bottom;
+// cy_l < 0: rows ly..ly+|cy_l|-1 at the top), one per lane.  Offsets relative
+// to s0 + b·P0 - ya (bottom) or s0 + b·P0 - ya + ly (top); the strip layout
+// guarantees every copy lies inside its window (strip_ya).
+constexpr int NVROW = 26;
+struct VRowTab {
+  int2 bot[32], top[32];  // (dst, src) offsets; entries >= NVROW unused
+};
+template <int NB, int P0>
+constexpr VRowTab make_vrows() {
+  VRowTab t{};
+  int nb = 0, nt = 0;
   for (int l = 0; l < Q; ++l) {
-    const int c = CY(l);
-    if (c == 0) continue;
-    // pointers indexed by absolute row
-    double* d = s0 + (l * NB + b) * P0 - ya - A0(l);
-    const double* m = s0 + (REFL(l) * NB + b) * P0 - ya - A0(REFL(l));
-    if (c > 0 && bottom) {
-      const int wbeg = ya + A0(l);  // first row of the window
-#pragma unroll
-      for (int q = 1; q <= 3; ++q)
-        if (q <= c && -q >= wbeg) d[-q] = m[q - 1];  // row -q <- refl row q - 1
-    }
-    if (c < 0 && top) {
-      const int wend = ya + A0(l) + R0;  // first row past the window
-#pragma unroll
-      for (int q = 0; q < 3; ++q)
-        if (q < -c && ly + q < wend) d[ly + q] = m[ly - 1 - q];  // row ly + q <- refl row ly - 1 - q
-    }
+    const int c = CY(l), m = REFL(l);
+    for (int q = 1; q <= c; ++q)  // row -q <- refl row q - 1
+      t.bot[nb++] = int2{l * NB * P0 - A0(l) - q, m * NB * P0 - A0(m) + q - 1};
+    for (int q = 0; q < -c; ++q)  // row ly + q <- refl row ly - 1 - q
+      t.top[nt++] = int2{l * NB * P0 - A0(l) + q, m * NB * P0 - A0(m) - 1 - q};
   }
+  return t;
+}
+template <int NB, int P0>
+constexpr bool vrows_ok() {
+  int nb = 0, nt = 0;
+  for (int l = 0; l < Q; ++l) {
+    nb += CY(l) > 0 ? CY(l) : 0;
+    nt += CY(l) < 0 ? -CY(l) : 0;
+  }
+  return nb == NVROW && nt == NVROW;
 }
 
 // Phase 1 site update: state n+1 at row y = ya - 3 + i from state-n buffer b
@@ -255,6 +261,12 @@ __device__ __forceinline__ void phase2(const double* s1, double* __restrict__ B,
     for (int l = 0; l < Q; ++l) q[l * nyp] = f[l];
   }
 }
+
+constexpr int TB_HT = 104;
+constexpr int TB_PF = 1;
+using Cfg = TbCfg<TB_HT, TB_PF>;
+static_assert(vrows_ok<Cfg::NB, Cfg::P0>(), "virtual-row copy count");
+__constant__ VRowTab c_vrows = make_vrows<Cfg::NB, Cfg::P0>();
 
 // Warps [0, NW1): phase 1; [NW1, NW1 + NW2): phase 2.
 template <int COLL, int HT, int PF>
@@ -348,7 +360,18 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
           // the warps that pull across a wall fill the virtual rows themselves
           // (redundantly if two do: same values) before reading them
           if (vbottom || vtop) {
-            if ((tid & 31) == 0) s0_virtual_rows<NB, P0, R0>(s0, buf, ya, ly, vbottom, vtop);
+            const int lane = tid & 31;
+            if (lane < NVROW) {
+              double* sb = s0 + buf * P0 - ya;
+              if (vbottom) {
+                const int2 e = c_vrows.bot[lane];
+                sb[e.x] = sb[e.y];
+              }
+              if (vtop) {
+                const int2 e = c_vrows.top[lane];
+                sb[ly + e.x] = sb[ly + e.y];
+              }
+            }
             __syncwarp();
           }
           const int i = tid;
@@ -388,9 +411,7 @@ bool encode(CUtensorMap* m, double* base, const Geo& g, int box_rows, int box_po
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-constexpr int TB_HT = 104;
-constexpr int TB_PF = 1;
-using Cfg = TbCfg<TB_HT, TB_PF>;
+
 
 template <int COLL>
 cudaError_t launch_tb(const Geo& g, const TbMaps* t, int src_buf, double* B, const Relax& r, int grid,
