@@ -314,14 +314,16 @@ int lb_sync(lb_ctx* ctx);
  * in shared memory (temporal blocking).  Bit-identical to two
  * fused steps; an odd remainder takes one fused step.  LB_OPT_TB_GRID: CTAs of
  * that kernel (0 = one per SM), LB_OPT_TB_L2_PREFETCH: L2 prefetch distance in
- * columns (0 = off, <= 64). */
+ * columns (0 = off, <= 64).  LB_OPT_TB_WALL_WEIGHT: cost of a column of a
+ * wall strip relative to an interior one, x16 (work split; default 20). */
 enum lb_option {
   LB_OPT_PROPAGATE_IMPL = 0,
   LB_OPT_FUSED_IMPL = 1,
   LB_OPT_CUDA_GRAPH = 2,
   LB_OPT_TEMPORAL = 3,
   LB_OPT_TB_GRID = 4,
-  LB_OPT_TB_L2_PREFETCH = 5
+  LB_OPT_TB_L2_PREFETCH = 5,
+  LB_OPT_TB_WALL_WEIGHT = 6
 };
 int lb_set_option(lb_ctx* ctx, int option, int value);
 

@@ -147,6 +147,7 @@ struct lb_ctx {
   int tb_on = 0;                // LB_OPT_TEMPORAL: two steps per pass where possible
   int tb_grid = 0;              // LB_OPT_TB_GRID: CTAs of the two-step kernel (0 = SM count)
   int tb_l2 = 0;                // LB_OPT_TB_L2_PREFETCH: L2 prefetch distance in columns
+  int tb_wall_w16 = 20;         // LB_OPT_TB_WALL_WEIGHT: wall-strip column cost x16 (work split)
   int sm_count = 148;
   cudaGraphExec_t gexec[2] = {nullptr, nullptr};  // keyed by the parity at graph start
   int gkey[2] = {-1, -1};       // configuration each graph was captured for
@@ -792,7 +793,7 @@ static int step_tb(lb_ctx* c) {
   const int grid = c->tb_grid > 0 ? c->tb_grid : c->sm_count;
   TRY(launch(c, c->p.collision ? "k_step2_tb_reg" : "k_step2_tb", c->s, 2 * c->L.sites, [&] {
     return lbk::launch_step2_tb(c->g, c->tb, c->par, c->B, c->p.bc_y, c->p.collision, c->relax, grid, c->tb_l2,
-                                c->s);
+                                c->tb_wall_w16, c->s);
   }));
   swap_ab(c);  // B held state n + 2: it becomes A
   c->halo_fresh = true;  // the kernel stored the border columns into B's halo
@@ -1022,6 +1023,10 @@ int lb_set_option(lb_ctx* c, int option, int value) {
     case LB_OPT_TB_L2_PREFETCH:
       if (value < 0 || value > 64) return fail(LB_EINVAL, "L2 prefetch distance must be in [0, 64]");
       c->tb_l2 = value;
+      return LB_OK;
+    case LB_OPT_TB_WALL_WEIGHT:
+      if (value < 1 || value > 256) return fail(LB_EINVAL, "wall weight (x16) must be in [1, 256]");
+      c->tb_wall_w16 = value;
       return LB_OK;
     case LB_OPT_FUSED_IMPL:
       if (value != 0 && value != 1) return fail(LB_EINVAL, "fused impl must be 0 (gather) or 1 (TMA)");

@@ -272,7 +272,7 @@ __constant__ VRowTab c_vrows = make_vrows<Cfg::NB, Cfg::P0>();
 template <int COLL, int HT, int PF>
 __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
     k_step2_tb(const __grid_constant__ CUtensorMap src, const __grid_constant__ CUtensorMap pf_map,
-               double* __restrict__ B, Geo g, Relax r, int nstrips, int l2_dist, int thermal) {
+               double* __restrict__ B, Geo g, Relax r, int nstrips, int l2_dist, int thermal, int wall_w16) {
   using C = TbCfg<HT, PF>;
   constexpr int R0 = C::R0, P0 = C::P0, R1 = C::R1, NB = C::NB;
   extern __shared__ __align__(128) double sm[];
@@ -289,9 +289,25 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
   }
   __syncthreads();
 
-  const int64_t U = (int64_t)nstrips * lx;
-  int64_t u = U * blockIdx.x / gridDim.x;
-  const int64_t u_end = U * (blockIdx.x + 1) / gridDim.x;
+  // Weighted split: a column of a wall strip costs wall_w16 / 16 of an interior
+  // one (thermal repopulation and mirror copies on its wall warps), so the CTAs
+  // that sweep wall strips get proportionally fewer columns.  unit_at(T): the
+  // first (strip, column) unit whose weighted start is >= T.
+  auto strip_w = [&](int s) { return (nstrips > 1 && (s == 0 || s == nstrips - 1)) ? wall_w16 : 16; };
+  auto unit_at = [&](int64_t T) -> int64_t {
+    int64_t acc = 0;
+    for (int s = 0; s < nstrips; ++s) {
+      const int w = strip_w(s);
+      const int64_t sw = (int64_t)lx * w;
+      if (T < acc + sw) return (int64_t)s * lx + (T - acc + w - 1) / w;
+      acc += sw;
+    }
+    return (int64_t)nstrips * lx;
+  };
+  int64_t wtot = 0;
+  for (int s = 0; s < nstrips; ++s) wtot += (int64_t)lx * strip_w(s);
+  int64_t u = unit_at(wtot * blockIdx.x / gridDim.x);
+  const int64_t u_end = unit_at(wtot * (blockIdx.x + 1) / gridDim.x);
   uint32_t kglob = 0;  // load iterations of this CTA over all its sweeps (barrier phase)
 
   while (u < u_end) {
@@ -415,7 +431,7 @@ bool encode(CUtensorMap* m, double* base, const Geo& g, int box_rows, int box_po
 
 template <int COLL>
 cudaError_t launch_tb(const Geo& g, const TbMaps* t, int src_buf, double* B, const Relax& r, int grid,
-                      int l2_dist, int thermal, cudaStream_t s) {
+                      int l2_dist, int thermal, int wall_w16, cudaStream_t s) {
   auto kern = k_step2_tb<COLL, TB_HT, TB_PF>;
   static unsigned long long done_mask = 0;  // opt-in smem is a per-device attribute
   int dev = 0;
@@ -429,7 +445,8 @@ cudaError_t launch_tb(const Geo& g, const TbMaps* t, int src_buf, double* B, con
   const int nstrips = (g.ly + TB_HT - 1) / TB_HT;
   const int64_t U = (int64_t)nstrips * g.lx;
   const int G = (int)std::min<int64_t>(grid, U);
-  kern<<<G, Cfg::NT, Cfg::SMEM, s>>>(t->load[src_buf], t->pf[src_buf], B, g, r, nstrips, l2_dist, thermal);
+  kern<<<G, Cfg::NT, Cfg::SMEM, s>>>(t->load[src_buf], t->pf[src_buf], B, g, r, nstrips, l2_dist, thermal,
+                                     wall_w16);
   return cudaGetLastError();
 }
 
@@ -462,11 +479,12 @@ cudaError_t tb_upload_constants(const double* k_bottom, const double* k_top, con
 }
 
 cudaError_t launch_step2_tb(const Geo& g, const TbMaps* t, int src_buf, double* B, int bc, int coll,
-                            const Relax& r, int grid, int l2_dist, cudaStream_t s) {
+                            const Relax& r, int grid, int l2_dist, int wall_w16, cudaStream_t s) {
   if (bc != BC_THERMAL && bc != BC_ADIABATIC) return cudaErrorNotSupported;
   const int thermal = bc == BC_THERMAL;
-  return coll == COLL_REGULARIZED ? launch_tb<COLL_REGULARIZED>(g, t, src_buf, B, r, grid, l2_dist, thermal, s)
-                                  : launch_tb<COLL_BGK>(g, t, src_buf, B, r, grid, l2_dist, thermal, s);
+  return coll == COLL_REGULARIZED
+             ? launch_tb<COLL_REGULARIZED>(g, t, src_buf, B, r, grid, l2_dist, thermal, wall_w16, s)
+             : launch_tb<COLL_BGK>(g, t, src_buf, B, r, grid, l2_dist, thermal, wall_w16, s);
 }
 
 }  // namespace lbk

@@ -424,13 +424,15 @@ class Lattice:
         """Replay 2-step CUDA graphs in lb_step (needs a non-default stream)."""
         _check(lib().lb_set_option(self._ctx, 2, int(enable)))
 
-    def temporal(self, enable: bool = True, grid: int = 0, l2_prefetch: int = 0):
+    def temporal(self, enable: bool = True, grid: int = 0, l2_prefetch: int = 0, wall_weight16: int = 20):
         """Two steps per pass over HBM (LB_OPT_TEMPORAL; N = 1, walls, monitors off):
         lb_step advances pairs of steps with the two-step kernel.  grid: CTAs
-        (0 = one per SM); l2_prefetch: L2 prefetch distance in columns (0 = off)."""
+        (0 = one per SM); l2_prefetch: L2 prefetch distance in columns (0 = off);
+        wall_weight16: cost of a wall-strip column, x16, for the work split."""
         _check(lib().lb_set_option(self._ctx, 3, int(enable)))
         _check(lib().lb_set_option(self._ctx, 4, int(grid)))
         _check(lib().lb_set_option(self._ctx, 5, int(l2_prefetch)))
+        _check(lib().lb_set_option(self._ctx, 6, int(wall_weight16)))
 
     def monitor(self, enable: bool = True):
         """Fused monitors: invariants reduced inside the step kernel (lb_monitor)."""

@@ -17,11 +17,11 @@ import lbgen  # noqa: E402
 import paper_1703_00186_b200 as lbm  # noqa: E402
 
 
-def run(lx, ly, tb, grid=0, l2=0, k=200, coll="bgk"):
+def run(lx, ly, tb, grid=0, l2=0, k=200, coll="bgk", ww=20):
     s = torch.cuda.Stream()
     g = lbm.Lattice(lx, ly, collision=coll, stream=s)
     if tb:
-        g.temporal(True, grid=grid, l2_prefetch=l2)
+        g.temporal(True, grid=grid, l2_prefetch=l2, wall_weight16=ww)
     g.init_macro(*lbgen.rt_macro(lx, ly, 1.0 / 1.19697977039307435897239 ** 2))
     g.step(20)
     g.sync()
@@ -51,6 +51,10 @@ def main():
             res.append({"tb": 1, "grid": grid, "l2": l2, "ms_per_step": ms, "mlups": ml,
                         "bit_identical": bool(np.array_equal(out, ref))})
             print(json.dumps(res[-1]), flush=True)
+    for ww in [int(x) for x in os.environ.get("TB_WW", "").split(",") if x]:
+        ms, ml, out = run(lx, ly, True, 0, 0, ww=ww)
+        print(json.dumps({"tb": 1, "wall_w16": ww, "ms_per_step": ms, "mlups": ml,
+                          "bit_identical": bool(np.array_equal(out, ref))}), flush=True)
     for coll in ("regularized",):
         ms, ml, ref = run(lx, ly, False, coll=coll)
         print(json.dumps({"tb": 0, "coll": coll, "mlups": ml}), flush=True)
