@@ -185,13 +185,13 @@ def kernel_passes(lb, lx_total, ly, fields, hbm_peak, fp64_peak, ncu, nsteps=10)
     regularised steps on the same workload (library instrumentation)."""
     kern = {}
     for mode, coll, impl in (("split", "bgk", "ldg"), ("split", "bgk", "tma"), ("fused", "bgk", "tma"),
-                             ("fused", "regularized", "ldg"), ("split", "regularized", "ldg"), ("fused", "bgk", "tb")):
-        g = lb.Lattice(lx_total, ly, mode=mode, collision=coll)
+                             ("fused", "regularized", "ldg"), ("split", "regularized", "ldg"), ("fused", "bgk", "ldg"),
+                             ("fused", "regularized", "tb")):
+        # "tb": the two-step kernel (the default path); the others pin the one-step kernels
+        g = lb.Lattice(lx_total, ly, mode=mode, collision=coll, temporal=(impl == "tb"))
         if mode == "split":
             g.set_propagate_impl(impl)
-        elif impl == "tb":
-            g.temporal(True)  # two steps per launch (k_step2_tb), an option: see DESIGN.md §8
-        else:
+        elif impl != "tb":
             g.set_fused_impl(impl)
         g.init_macro(*fields)
         g.step(3)
@@ -218,7 +218,7 @@ def kernel_passes(lb, lx_total, ly, fields, hbm_peak, fp64_peak, ncu, nsteps=10)
                     e.update({"flops_per_site_ncu": fl, "fp64_tflops": tf, "fp64_frac": tf / fp64_peak,
                               "fp64_peak_tflops": fp64_peak})
                 e["paper_convention_6500_flop_tflops"] = 6500 * e["mlups"] * 1e6 / 1e12
-            if k == "k_step2_tb":
+            if k.startswith("k_step2_tb"):
                 # one launch = two time steps; algorithmic HBM traffic = one read + one
                 # write of the state (592 B/site) per launch
                 e["site_updates_per_launch"] = v["units"] / v["launches"]
@@ -358,10 +358,13 @@ def main():
     fp64 = load_json(os.path.join(ROOT, "profiles", "r01_fp64_hbm_microbench.json"), {}) or {}
     fp64_peak = fp64.get("fp64_tflops")
 
-    # dominant kernel: every launch of k_step_fused (whole lattice, or bulk +
-    # border launches of the overlapped schedule), aggregated
-    parts = [v for k, v in prof.items() if k.startswith("k_step_fused") and "_reg" not in k]
-    kname = "k_step_fused"
+    # dominant kernel: the two-step kernel k_step2_tb (the default N = 1 path),
+    # else every launch of k_step_fused (whole lattice, or bulk + border
+    # launches of the overlapped schedule), aggregated
+    two_step = "k_step2_tb" in prof
+    kname = "k_step2_tb" if two_step else "k_step_fused"
+    parts = [v for k, v in prof.items() if k == kname] if two_step else \
+        [v for k, v in prof.items() if k.startswith("k_step_fused") and "_reg" not in k]
     fk = {"launches": sum(v["launches"] for v in parts), "total_ms": sum(v["total_ms"] for v in parts),
           "units": sum(v["units"] for v in parts)} if parts else None
     if fk and world > 1:
@@ -370,19 +373,29 @@ def main():
     roofline = None
     if fk and fk["launches"]:
         avg_ms = fk["total_ms"] / fk["launches"]
-        bytes_per_launch = BYTES_PER_SITE * fk["units"] / fk["launches"]
-        achieved = pm.gbs(fk["units"] / fk["launches"], avg_ms * 1e-3)   # sites x 592 B / t
+        # algorithmic bytes of one launch: one read + one write of the state
+        # (592 B/site) -- per step for k_step_fused, per TWO steps for
+        # k_step2_tb (its units are site updates: 2 x sites per launch)
+        sites_per_launch = fk["units"] / fk["launches"] / (2 if two_step else 1)
+        bytes_per_launch = BYTES_PER_SITE * sites_per_launch
+        achieved = pm.gbs(sites_per_launch, avg_ms * 1e-3)   # sites x 592 B / t
         kn = ncu.get("kernels", {}).get(kname, {})
         traffic = kn.get("dram_bytes_per_site")
         roofline = {"kernel": kname, "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak,
                     "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
-                    "traffic": (traffic * fk["units"] / fk["launches"]) if traffic else None,
+                    "traffic": (traffic * sites_per_launch) if traffic else None,
                     "algorithmic_bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_ms,
                     "share_of_step": fk["total_ms"] / ms_prof,
                     "measured": "per-launch CUDA events on the launch stream over a second timed region "
                                 f"of the same {args.steps} steps",
                     "peak_source": peak_src,
                     "traffic_source": ncu.get("source") if traffic else None}
+        if two_step:
+            roofline["steps_per_launch"] = 2
+            roofline["one_step_equivalent_gbs"] = round(2 * achieved, 1)
+            roofline["note"] = ("two time steps per HBM pass (temporal blocking): achieved/frac count the "
+                                "592 B/site one pass moves; one_step_equivalent_gbs is the bandwidth a "
+                                "one-step kernel would need for the same MLUPS (DESIGN.md section 6)")
 
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "MLUPS", "n_gpus": world,
@@ -408,17 +421,33 @@ def main():
         st0 = g.peek(0)
         host_in.numpy()[:] = st0.reshape(-1)
         del st0
-        k_e2e = max(10, min(args.steps, 1000))   # the same K as the timed region
+        k_e2e = max(10, min(args.steps, 1000)) // 2 * 2   # the same K as the timed region
         g.monitor(True)   # per-step invariants reduced inside the step kernel (lb_monitor)
         mon = torch.empty((k_e2e, 5), dtype=torch.float64).pin_memory()   # per-step results on the host
+        # the two-step kernel (default at N = 1 with walls) carries monitors of
+        # BOTH its states: lb_step(2) + lb_invariants_pair_async still returns
+        # one result per time step
+        pair = False
+        try:
+            g.step(2)
+            g.invariants_pair_async(mon[0:2])
+            g.sync()
+            pair = True
+        except lb.LBError:
+            pass
         barrier()
         torch.cuda.synchronize()
         t = time.perf_counter()
         g.set_state(host_in.numpy())
         barrier()  # peer mode: neighbours' states set before the first halo pull
-        for k in range(k_e2e):
-            g.step(1)
-            g.invariants_async(mon[k])   # D2H of the step's result into pinned memory
+        if pair:
+            for k in range(0, k_e2e, 2):
+                g.step(2)
+                g.invariants_pair_async(mon[k:k + 2])   # D2H of both steps' results into pinned memory
+        else:
+            for k in range(k_e2e):
+                g.step(1)
+                g.invariants_async(mon[k])   # D2H of the step's result into pinned memory
         if same_gpu:
             g.peek(0)   # no communicator: each rank reads its own slab back
         else:
@@ -430,8 +459,11 @@ def main():
                        "h2d_bytes_per_step": state_bytes / k_e2e,
                        "d2h_bytes_per_step": (state_bytes + 5 * 8 * k_e2e) / k_e2e,
                        "steps": k_e2e, "mode": args.mode,
-                       "timed": "lb_set_state(pinned host) + K x (lb_step(1) with fused monitors + "
-                                "lb_invariants_async -> pinned host) + lb_gather(pinned host)",
+                       "timed": ("lb_set_state(pinned host) + K/2 x (lb_step(2) on the two-step kernel with "
+                                 "monitors of both states + lb_invariants_pair_async -> pinned host: one result "
+                                 "per step) + lb_gather(pinned host)") if pair else
+                                ("lb_set_state(pinned host) + K x (lb_step(1) with fused monitors + "
+                                 "lb_invariants_async -> pinned host) + lb_gather(pinned host)"),
                        "per_step_results_ok": bool(np.isfinite(m).all() and (m[:, 4] > 0).all()),
                        "mass_drift_over_K": mass_drift}
         del host_in, host_out

@@ -295,6 +295,14 @@ int lb_invariants(lb_ctx* ctx, double* out);
  * valid after the next lb_sync; no NaN / rho checks are made. */
 int lb_invariants_async(lb_ctx* ctx, double* host_out);
 
+/* Both states of the last two-step launch (LB_OPT_TEMPORAL) with monitors on:
+ * enqueues host_out[0..4] = the invariants (as lb_invariants) of state n+1 and
+ * host_out[5..9] = those of state n+2, reduced from per-CTA partials the
+ * two-step kernel wrote (so a two-step lb_step(2) still yields one result per
+ * time step).  host_out: 10 doubles, page-locked for true asynchrony; valid
+ * after the next lb_sync.  LB_ESTATE if the last step was not such a launch. */
+int lb_invariants_pair_async(lb_ctx* ctx, double* host_out);
+
 int lb_sync(lb_ctx* ctx);
 
 /* Options.  LB_OPT_PROPAGATE_IMPL (lb_propagate, split mode): 1 = TMA-staged
@@ -308,8 +316,9 @@ int lb_sync(lb_ctx* ctx);
  * steady state of the fused N = 1 path and of the peer path (bit-identical;
  * fewer host launches, matters for small lattices).  Needs a non-default
  * context stream; ignored while profiling. */
-/* LB_OPT_TEMPORAL (value 1): lb_step advances two steps per pass over HBM
- * where it can (N = 1 without NCCL or peers, walls, fused mode, monitors off):
+/* LB_OPT_TEMPORAL (value 1, the default for N = 1 with walls in fused mode;
+ * 0 disables): lb_step advances two steps per pass over HBM where it can
+ * (N = 1 without NCCL or peers, walls, fused mode, monitors off):
  * one launch of the two-step kernel computes states n+1 and n+2, keeping n+1
  * in shared memory (temporal blocking).  Bit-identical to two
  * fused steps; an odd remainder takes one fused step.  LB_OPT_TB_GRID: CTAs of

@@ -92,9 +92,13 @@ void tb_destroy(TbMaps* t);
 // lb_tb.cu's own copies of the wall constants and the Gram inverse
 cudaError_t tb_upload_constants(const double* k_bottom, const double* k_top, const double* ginv, cudaStream_t s);
 // grid: CTAs (one per SM); l2_dist: L2 prefetch distance in columns (0 = off);
-// wall_w16: cost of a wall-strip column in 1/16 of an interior one (work split)
+// wall_w16: cost of a wall-strip column in 1/16 of an interior one (work split);
+// mon != nullptr: monitors, 2 x tb_grid(g, grid) x 5 doubles of per-CTA
+// partials (state n+1, then state n+2)
 cudaError_t launch_step2_tb(const Geo& g, const TbMaps* t, int src_buf, double* B, int bc, int coll,
-                            const lbd::Relax& r, int grid, int l2_dist, int wall_w16, cudaStream_t s);
+                            const lbd::Relax& r, int grid, int l2_dist, int wall_w16, double* mon, cudaStream_t s);
+// CTAs a two-step launch with `grid` requested actually uses
+int tb_grid(const Geo& g, int grid);
 // this rank's counter += 1 (system-scope release), after the step kernel
 cudaError_t launch_signal(unsigned long long* done, cudaStream_t s);
 cudaError_t launch_peer_pull(const Geo& g, double* A, const double* left_A, const double* right_A,

@@ -204,12 +204,31 @@ constexpr bool vrows_ok() {
   return nb == NVROW && nt == NVROW;
 }
 
+// Monitors (lb_monitor): per-thread running sums of the invariants of the
+// sites a CTA owns (rho, j_x, j_y, E = 1/2 sum |c|^2 f, and min rho; a NaN
+// density counts as -inf so the minimum flags it).
+__device__ __forceinline__ void acc_invariants(const double (&f)[Q], double (&a)[5]) {
+  double rho = 0.0, jx = 0.0, jy = 0.0, e = 0.0;
+#pragma unroll
+  for (int l = 0; l < Q; ++l) {
+    rho = __dadd_rn(rho, f[l]);
+    jx = __fma_rn((double)CX(l), f[l], jx);
+    jy = __fma_rn((double)CY(l), f[l], jy);
+    e = __fma_rn(0.5 * (double)c2(l), f[l], e);
+  }
+  a[0] = __dadd_rn(a[0], rho);
+  a[1] = __dadd_rn(a[1], jx);
+  a[2] = __dadd_rn(a[2], jy);
+  a[3] = __dadd_rn(a[3], e);
+  a[4] = fmin(a[4], rho != rho ? -INFINITY : rho);
+}
+
 // Phase 1 site update: state n+1 at row y = ya - 3 + i from state-n buffer b
 // (the pulled values), result into the state-(n+1) ring slot of iteration t;
 // the rows next to a wall also write the virtual rows their values mirror into.
-template <int COLL, int NB, int P0, int R1>
+template <int COLL, int NB, int P0, int R1, bool MON>
 __device__ __forceinline__ void phase1(const double* s0, double* s1, int b, int t, int i, int y, int ly,
-                                       bool thermal, const Relax& r) {
+                                       bool thermal, const Relax& r, bool own, double (&acc)[5]) {
   double f[Q];
   const int io = opaque(i);  // not hoistable: no per-population address registers
   const double* sb = s0 + b * P0 + io;
@@ -221,6 +240,7 @@ __device__ __forceinline__ void phase1(const double* s0, double* s1, int b, int 
   else collide_site(f, r);
 #pragma unroll
   for (int l = 0; l < Q; ++l) s1[(SLOTS1_BEFORE(l) + (t % L1(l))) * R1 + io] = f[l];
+  if (MON && own) acc_invariants(f, acc);
   if (wall) {
     // virtual row of refl(l): -1 - y (bottom) or 2 ly - 1 - y (top); ring row
     // index = absolute row - (ya - 3), and i = y - (ya - 3)
@@ -234,9 +254,9 @@ __device__ __forceinline__ void phase1(const double* s0, double* s1, int b, int 
 
 // Phase 2 site update: state n+2 at row y = ya + i, column c2, from the
 // state-(n+1) ring, stored to B (+ B's halo for the 3+3 border columns).
-template <int COLL, int R1>
+template <int COLL, int R1, bool MON>
 __device__ __forceinline__ void phase2(const double* s1, double* __restrict__ B, const Geo& g, int t, int i,
-                                       int y, int c2, bool thermal, const Relax& r) {
+                                       int y, int c2, bool thermal, const Relax& r, bool own, double (&acc)[5]) {
   const int ly = g.ly;
   double f[Q];
   const int io = opaque(i);
@@ -245,6 +265,7 @@ __device__ __forceinline__ void phase2(const double* s1, double* __restrict__ B,
   if (thermal && (y < 3 || y >= ly - 3)) thermal_wall(f, y < 3 ? 0 : 1);
   if (COLL == COLL_REGULARIZED) collide_site_reg(f, r);
   else collide_site(f, r);
+  if (MON && own) acc_invariants(f, acc);
   const int nyp = opaque(g.nyp);
   double* p = B + (int64_t)c2 * g.cs + g.y0 + y;
 #pragma unroll
@@ -269,10 +290,15 @@ static_assert(vrows_ok<Cfg::NB, Cfg::P0>(), "virtual-row copy count");
 __constant__ VRowTab c_vrows = make_vrows<Cfg::NB, Cfg::P0>();
 
 // Warps [0, NW1): phase 1; [NW1, NW1 + NW2): phase 2.
-template <int COLL, int HT, int PF>
+// MON: monitors — each CTA reduces the invariants of the sites it owns (rows
+// of its strips not covered by a lower strip, its output columns) for state
+// n+1 into mon[blockIdx] and for state n+2 into mon[gridDim + blockIdx]
+// (5 doubles each; fixed-order reductions, deterministic).
+template <int COLL, int HT, int PF, bool MON>
 __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
     k_step2_tb(const __grid_constant__ CUtensorMap src, const __grid_constant__ CUtensorMap pf_map,
-               double* __restrict__ B, Geo g, Relax r, int nstrips, int l2_dist, int thermal, int wall_w16) {
+               double* __restrict__ B, Geo g, Relax r, int nstrips, int l2_dist, int thermal, int wall_w16,
+               double* __restrict__ mon) {
   using C = TbCfg<HT, PF>;
   constexpr int R0 = C::R0, P0 = C::P0, R1 = C::R1, NB = C::NB;
   extern __shared__ __align__(128) double sm[];
@@ -309,6 +335,7 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
   int64_t u = unit_at(wtot * blockIdx.x / gridDim.x);
   const int64_t u_end = unit_at(wtot * (blockIdx.x + 1) / gridDim.x);
   uint32_t kglob = 0;  // load iterations of this CTA over all its sweeps (barrier phase)
+  double acc[5] = {0.0, 0.0, 0.0, 0.0, INFINITY};  // MON: this thread's state (n+1 or n+2)
 
   while (u < u_end) {
     const int strip = (int)(u / lx);
@@ -322,6 +349,9 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
     const int nload = W + 6;          // phase-1 iterations (columns c1 = xs - 3 + t)
     const int niter = W + 7;          // + the phase-2 lag
     const int rbase = g.y0 + ya;      // internal row of ya
+    // MON: rows this strip owns (not covered by the strip below)
+    const int own_lo = strip == 0 ? 0 : std::max(ya, strip_ya(strip - 1, nstrips, ly, HT) + HT);
+    const int own_hi = std::min(ya + HT, ly);
     // phase-1 warp rows [ya - 3 + 32 w, +32): does it pull across a wall?
     const int wr0 = ya - 3 + 32 * warp, wr1 = std::min(wr0 + 32, ya + HT + 3);
     const bool vbottom = warp < C::NW1 && wr0 < 3 && wr1 > 0;
@@ -392,17 +422,48 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
           }
           const int i = tid;
           const int y = ya - 3 + i;
-          if (i < R1 && y >= 0 && y < ly) phase1<COLL, NB, P0, R1>(s0, s1, buf, t, i, y, ly, thermal, r);
+          if (i < R1 && y >= 0 && y < ly)
+            phase1<COLL, NB, P0, R1, MON>(s0, s1, buf, t, i, y, ly, thermal, r,
+                                          t >= 3 && t < W + 3 && y >= own_lo && y < own_hi, acc);
         }
       } else if (t >= 7) {
         // phase 2: state n+2 at column c2 = xs - 7 + t, rows [ya, ya+HT)
         const int i = tid - 32 * C::NW1;
         const int y = ya + i;
-        if (i < HT && y < ly) phase2<COLL, R1>(s1, B, g, t, i, y, xs - 7 + t, thermal, r);
+        if (i < HT && y < ly)
+          phase2<COLL, R1, MON>(s1, B, g, t, i, y, xs - 7 + t, thermal, r, y >= own_lo && y < own_hi, acc);
       }
     }
     kglob += (uint32_t)nload;
     __syncthreads();  // the next sweep refills every ring
+  }
+  if (MON) {
+    // warp xor-tree, then the warps of each phase in order (deterministic)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) acc[k] = __dadd_rn(acc[k], __shfl_xor_sync(0xffffffffu, acc[k], o));
+      acc[4] = fmin(acc[4], __shfl_xor_sync(0xffffffffu, acc[4], o));
+    }
+    double* red = s1;  // the rings are free now
+    if ((tid & 31) == 0)
+#pragma unroll
+      for (int k = 0; k < 5; ++k) red[warp * 5 + k] = acc[k];
+    __syncthreads();
+    if (tid < 2) {
+      const int w0 = tid == 0 ? 0 : C::NW1, w1 = tid == 0 ? C::NW1 : C::NW;
+      double v[5];
+#pragma unroll
+      for (int k = 0; k < 5; ++k) v[k] = red[w0 * 5 + k];
+      for (int w = w0 + 1; w < w1; ++w) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[k] = __dadd_rn(v[k], red[w * 5 + k]);
+        v[4] = fmin(v[4], red[w * 5 + 4]);
+      }
+      double* slot = mon + ((int64_t)(tid == 0 ? 0 : gridDim.x) + blockIdx.x) * 5;
+#pragma unroll
+      for (int k = 0; k < 5; ++k) slot[k] = v[k];
+    }
   }
 }
 
@@ -429,10 +490,10 @@ bool encode(CUtensorMap* m, double* base, const Geo& g, int box_rows, int box_po
 
 
 
-template <int COLL>
+template <int COLL, bool MON>
 cudaError_t launch_tb(const Geo& g, const TbMaps* t, int src_buf, double* B, const Relax& r, int grid,
-                      int l2_dist, int thermal, int wall_w16, cudaStream_t s) {
-  auto kern = k_step2_tb<COLL, TB_HT, TB_PF>;
+                      int l2_dist, int thermal, int wall_w16, double* mon, cudaStream_t s) {
+  auto kern = k_step2_tb<COLL, TB_HT, TB_PF, MON>;
   static unsigned long long done_mask = 0;  // opt-in smem is a per-device attribute
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -442,17 +503,19 @@ cudaError_t launch_tb(const Geo& g, const TbMaps* t, int src_buf, double* B, con
     if (e != cudaSuccess) return e;
     if (dev < 64) done_mask |= 1ull << dev;
   }
-  const int nstrips = (g.ly + TB_HT - 1) / TB_HT;
-  const int64_t U = (int64_t)nstrips * g.lx;
-  const int G = (int)std::min<int64_t>(grid, U);
-  kern<<<G, Cfg::NT, Cfg::SMEM, s>>>(t->load[src_buf], t->pf[src_buf], B, g, r, nstrips, l2_dist, thermal,
-                                     wall_w16);
+  kern<<<tb_grid(g, grid), Cfg::NT, Cfg::SMEM, s>>>(t->load[src_buf], t->pf[src_buf], B, g, r,
+                                                    (g.ly + TB_HT - 1) / TB_HT, l2_dist, thermal, wall_w16, mon);
   return cudaGetLastError();
 }
 
 }  // namespace
 
 bool tb_layout_ok(int ly) { return ly <= TB_HT || ly >= TB_HT + 6; }
+
+int tb_grid(const Geo& g, int grid) {
+  const int64_t U = (int64_t)((g.ly + TB_HT - 1) / TB_HT) * g.lx;
+  return (int)std::min<int64_t>(grid, U);
+}
 
 TbMaps* tb_create(const Geo& g, double* buf0, double* buf1) {
   if (g.y0 % 2 || g.nyp % 2 || g.lx < 2 * H) return nullptr;
@@ -479,12 +542,16 @@ cudaError_t tb_upload_constants(const double* k_bottom, const double* k_top, con
 }
 
 cudaError_t launch_step2_tb(const Geo& g, const TbMaps* t, int src_buf, double* B, int bc, int coll,
-                            const Relax& r, int grid, int l2_dist, int wall_w16, cudaStream_t s) {
+                            const Relax& r, int grid, int l2_dist, int wall_w16, double* mon, cudaStream_t s) {
   if (bc != BC_THERMAL && bc != BC_ADIABATIC) return cudaErrorNotSupported;
-  const int thermal = bc == BC_THERMAL;
+  const int th = bc == BC_THERMAL;
+  if (mon)
+    return coll == COLL_REGULARIZED
+               ? launch_tb<COLL_REGULARIZED, true>(g, t, src_buf, B, r, grid, l2_dist, th, wall_w16, mon, s)
+               : launch_tb<COLL_BGK, true>(g, t, src_buf, B, r, grid, l2_dist, th, wall_w16, mon, s);
   return coll == COLL_REGULARIZED
-             ? launch_tb<COLL_REGULARIZED>(g, t, src_buf, B, r, grid, l2_dist, thermal, wall_w16, s)
-             : launch_tb<COLL_BGK>(g, t, src_buf, B, r, grid, l2_dist, thermal, wall_w16, s);
+             ? launch_tb<COLL_REGULARIZED, false>(g, t, src_buf, B, r, grid, l2_dist, th, wall_w16, mon, s)
+             : launch_tb<COLL_BGK, false>(g, t, src_buf, B, r, grid, l2_dist, th, wall_w16, mon, s);
 }
 
 }  // namespace lbk

@@ -30,7 +30,7 @@ EXPORTS = ["lb_query_layout", "lb_exchange_plan", "lb_constants", "lb_kwall", "l
            "lb_set_state", "lb_exchange", "lb_propagate", "lb_bc", "lb_collide", "lb_step",
            "lb_gather", "lb_peek", "lb_invariants", "lb_sync", "lb_profile_enable",
            "lb_profile_reset", "lb_profile_read", "lb_launch_count", "lb_set_peers",
-           "lb_monitor", "lb_peek_cols", "lb_set_option", "lb_invariants_async"]
+           "lb_monitor", "lb_peek_cols", "lb_set_option", "lb_invariants_async", "lb_invariants_pair_async"]
 
 
 class LBError(RuntimeError):
@@ -112,6 +112,7 @@ def lib():
         "lb_peek_cols": (i, [vp, i, i, i, vp]),
         "lb_invariants": (i, [vp, vp]),
         "lb_invariants_async": (i, [vp, vp]),
+        "lb_invariants_pair_async": (i, [vp, vp]),
         "lb_sync": (i, [vp]),
         "lb_profile_enable": (i, [vp, i]), "lb_profile_reset": (i, [vp]),
         "lb_profile_read": (i, [vp, p(lb_kprof), i, p(i)]),
@@ -200,7 +201,7 @@ class Lattice:
 
     def __init__(self, lx_total, ly, tau=0.8, dt=1.0, t_bottom=None, t_top=None, bc_y="thermal",
                  mode="fused", overlap=False, rank=0, nranks=1, nccl_id: bytes | None = None,
-                 device=None, stream=None, collision="bgk", gravity=(0.0, 0.0)):
+                 device=None, stream=None, collision="bgk", gravity=(0.0, 0.0), temporal=None):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("paper_1703_00186_b200 needs a CUDA device (no CPU fallback)")
@@ -221,6 +222,8 @@ class Lattice:
                                  ctypes.c_void_p(self.bufs[1].data_ptr()),
                                  ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(ctx)))
         self._ctx = ctx
+        if temporal is not None:   # None: the library default (two-step kernel where it applies)
+            _check(lib().lb_set_option(self._ctx, 3, int(bool(temporal))))
 
     # lifetime
     def close(self):
@@ -332,6 +335,18 @@ class Lattice:
             ptr = _dptr(out)
         _check(lib().lb_invariants_async(self._ctx, ptr))
 
+    def invariants_pair_async(self, out) -> None:
+        """After a two-step lb_step(2) with monitors: enqueue the invariants of
+        both states into `out` (10 float64: state n+1, then n+2); valid after sync()."""
+        import torch
+        if isinstance(out, torch.Tensor):
+            assert out.dtype == torch.float64 and out.numel() >= 10 and not out.is_cuda and out.is_contiguous()
+            ptr = ctypes.c_void_p(out.data_ptr())
+        else:
+            assert out.size >= 10 and out.dtype == np.float64
+            ptr = _dptr(out)
+        _check(lib().lb_invariants_pair_async(self._ctx, ptr))
+
     def peek_cols(self, x0: int, ncols: int, which: int = 0) -> np.ndarray:
         """Local physical columns [x0, x0+ncols) of A (0) or B (1): [37][ncols][ly]."""
         out = np.empty((Q, ncols, self.ly))
@@ -425,7 +440,8 @@ class Lattice:
         _check(lib().lb_set_option(self._ctx, 2, int(enable)))
 
     def temporal(self, enable: bool = True, grid: int = 0, l2_prefetch: int = 0, wall_weight16: int = 20):
-        """Two steps per pass over HBM (LB_OPT_TEMPORAL; N = 1, walls, monitors off):
+        """Two steps per pass over HBM (LB_OPT_TEMPORAL, the default where it
+        applies: N = 1, walls, fused mode, monitors off):
         lb_step advances pairs of steps with the two-step kernel.  grid: CTAs
         (0 = one per SM); l2_prefetch: L2 prefetch distance in columns (0 = off);
         wall_weight16: cost of a wall-strip column, x16, for the work split."""

@@ -120,18 +120,21 @@ def test_collide_parity(lb, tau):
 
 # ------------------------------------------------------------------ trajectories (config #1)
 
-@pytest.mark.parametrize("mode,overlap", [("split", False), ("fused", False), ("fused", True)])
+@pytest.mark.parametrize("mode,overlap,stride", [("split", False, 1), ("fused", False, 1), ("fused", True, 1),
+                                                 ("fused", False, 2)])
 @pytest.mark.parametrize("bc", ["thermal", "adiabatic", "periodic"])
-def test_trajectory_64x32_10_steps(lb, mode, overlap, bc):
-    """Config #1: 64x32, RT init on each side, 10 steps, compared after every step."""
+def test_trajectory_64x32_10_steps(lb, mode, overlap, stride, bc):
+    """Config #1: 64x32, RT init on each side, 10 steps, compared after every step
+    (stride 1: the one-step kernels) or every second step (stride 2, fused: the
+    two-step kernel, the default for walls at N = 1)."""
     lx, ly = 64, 32
     g, o = pair(lb, lx, ly, bc=bc, mode=mode, overlap=overlap)
     fields = lbgen.rt_macro(lx, ly, oracle.t0())
     g.init_macro(*fields)
     o.init_macro(*fields)
-    for k in range(10):
-        g.step(1)
-        o.step(1)
+    for k in range(10 // stride):
+        g.step(stride)
+        o.step(stride)
         err = max_rel(g.gather(), o.get_state(0))
         assert err < TOL, (k, err)
     inv_g = g.invariants()
@@ -578,7 +581,7 @@ def test_tma_fused_step_bit_identical(lb, coll, bc, shape):
     st = oracle_state(lx, ly, seed=lx + ly)
     outs = []
     for impl in ("ldg", "tma"):
-        g = lb.Lattice(lx, ly, bc_y=bc, collision=coll, gravity=(0.0, -1e-5))
+        g = lb.Lattice(lx, ly, bc_y=bc, collision=coll, gravity=(0.0, -1e-5), temporal=False)
         g.set_fused_impl(impl)
         g.set_state(st)
         g.step(5)
@@ -641,6 +644,53 @@ def test_two_step_kernel_oracle_parity(lb):
     assert max_rel(g.gather(), o.get_state(0)) < TOL
 
 
+@pytest.mark.parametrize("coll", ["bgk", "regularized"])
+@pytest.mark.parametrize("shape", [(64, 32), (40, 150), (9, 211), (17, 131)])
+def test_two_step_kernel_monitors(lb, coll, shape):
+    """Monitors inside the two-step kernel: both states' invariants (owned rows
+    and columns, each site once) equal full-pass invariants to 1e-13, the state
+    is bit-identical to monitors off, and grids of 1..300 CTAs agree."""
+    lx, ly = shape
+    st = oracle_state(lx, ly, seed=lx + 3 * ly)
+    ref = lb.Lattice(lx, ly, collision=coll)
+    ref.set_state(st)
+    full = []
+    for _ in range(2):
+        ref.step(1)
+        full.append(ref.invariants())
+    for grid in (0, 1, 7, 300):
+        g = lb.Lattice(lx, ly, collision=coll)
+        g.temporal(True, grid=grid)
+        g.monitor(True)
+        g.set_state(st)
+        g.step(2)
+        pair_out = np.zeros(10)
+        g.invariants_pair_async(pair_out)
+        g.sync()
+        latest = g.invariants()
+        for k in range(2):
+            got, want = pair_out[5 * k:5 * k + 5], full[k]
+            assert abs(got[0] - want[0]) <= 1e-13 * want[0], (grid, k)
+            assert np.allclose(got[1:4], want[1:4], rtol=1e-12, atol=1e-13 * want[0]), (grid, k)
+            assert abs(got[4] - want[4]) <= 1e-14 * want[4], (grid, k)
+        assert np.array_equal(latest, pair_out[5:])
+        assert np.array_equal(g.gather(), ref.gather())
+        g.close()
+
+
+def test_two_step_pair_invariants_state_errors(lb):
+    g = lb.Lattice(40, 60)
+    g.monitor(True)
+    g.init_macro(*lbgen.rt_macro(40, 60, oracle.t0()))
+    with pytest.raises(lb.LBError):
+        g.invariants_pair_async(np.zeros(10))   # no two-step launch yet
+    g.step(1)
+    with pytest.raises(lb.LBError):
+        g.invariants_pair_async(np.zeros(10))   # last step was a one-step launch
+    g.step(2)
+    g.invariants_pair_async(np.zeros(10))
+
+
 # ------------------------------------------------------------------ CUDA-graph stepping
 
 @pytest.mark.parametrize("coll,monitor", [("bgk", False), ("regularized", True)])
@@ -649,7 +699,7 @@ def test_graph_steps_bit_identical(lb, coll, monitor):
     st = oracle_state(lx, ly, seed=77)
     outs, invs = [], []
     for graphs in (False, True):
-        g = lb.Lattice(lx, ly, collision=coll, stream=torch.cuda.Stream())
+        g = lb.Lattice(lx, ly, collision=coll, stream=torch.cuda.Stream(), temporal=False)
         if graphs:
             g.use_graphs(True)
         if monitor:

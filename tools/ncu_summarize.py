@@ -25,7 +25,7 @@ for r in rows:
     base = name.split("<")[0]
     targs = name[len(base):].strip("<>").replace(" ", "").split(",") if "<" in name else []
     # collision kind: k_step_fused<BC, COLL, MON> / k_collide<COLL>
-    coll_arg = {"k_step_fused": 1, "k_collide": 0}.get(base)
+    coll_arg = {"k_step_fused": 1, "k_collide": 0, "k_step2_tb": 0}.get(base)
     if coll_arg is not None and len(targs) > coll_arg and targs[coll_arg] == "1":
         base += "_reg"
     if base.startswith("k_step_fused") and len(targs) > 2 and targs[2] in ("1", "true"):

@@ -1,6 +1,7 @@
 """Small target for ncu: a few steps per spec at 1920x2048.
 
-spec = mode[:collision[:impl]]   e.g.  fused  split  fused:regularized  split:bgk:ldg  fused:bgk:tma
+spec = mode[:collision[:impl]]   e.g.  fused  split  fused:regularized  split:bgk:ldg  fused:bgk:tma  fused:bgk:tb
+(fused specs without impl "tb" run the one-step kernel; "tb" the two-step kernel)
 ncu ... python tools/ncu_target.py fused split fused:regularized split:regularized split:bgk:ldg
 """
 import os
@@ -19,11 +20,11 @@ for spec in sys.argv[1:] or ["fused", "split"]:
     mode = parts[0]
     coll = parts[1] if len(parts) > 1 else "bgk"
     impl = parts[2] if len(parts) > 2 else None
-    g = lb.Lattice(lx, ly, mode=mode, collision=coll)
-    if impl:
+    g = lb.Lattice(lx, ly, mode=mode, collision=coll, temporal=(impl == "tb"))
+    if impl and impl != "tb":
         (g.set_propagate_impl if mode == "split" else g.set_fused_impl)(impl)
     g.init_macro(*fields)
-    g.step(3)
+    g.step(4 if impl == "tb" else 3)
     g.sync()
     g.close()
     del g

@@ -19,7 +19,7 @@ import paper_1703_00186_b200 as lbm  # noqa: E402
 
 def run(lx, ly, tb, grid=0, l2=0, k=200, coll="bgk", ww=20):
     s = torch.cuda.Stream()
-    g = lbm.Lattice(lx, ly, collision=coll, stream=s)
+    g = lbm.Lattice(lx, ly, collision=coll, stream=s, temporal=False)
     if tb:
         g.temporal(True, grid=grid, l2_prefetch=l2, wall_weight16=ww)
     g.init_macro(*lbgen.rt_macro(lx, ly, 1.0 / 1.19697977039307435897239 ** 2))

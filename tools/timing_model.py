@@ -21,7 +21,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 
 def kernel_ms(lb, lbgen, lx, ly, steps=20, **kw):
-    g = lb.Lattice(lx, ly, **kw)
+    g = lb.Lattice(lx, ly, temporal=False, **kw)  # the one-step kernel (the multi-GPU path)
     g.init_macro(*lbgen.rt_macro(lx, ly, lb.t0()))
     g.step(3)
     g.profile(True)
