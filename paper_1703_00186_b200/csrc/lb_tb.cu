@@ -352,10 +352,9 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
     // MON: rows this strip owns (not covered by the strip below)
     const int own_lo = strip == 0 ? 0 : std::max(ya, strip_ya(strip - 1, nstrips, ly, HT) + HT);
     const int own_hi = std::min(ya + HT, ly);
-    // phase-1 warp rows [ya - 3 + 32 w, +32): does it pull across a wall?
-    const int wr0 = ya - 3 + 32 * warp, wr1 = std::min(wr0 + 32, ya + HT + 3);
-    const bool vbottom = warp < C::NW1 && wr0 < 3 && wr1 > 0;
-    const bool vtop = warp < C::NW1 && wr1 > ly - 3 && wr0 < ly;
+    // do phase-1 rows [ya - 3, ya + HT + 3) pull across a wall (CTA-uniform)?
+    const bool vbottom = ya - 3 < 3;
+    const bool vtop = ya + HT + 3 > ly - 3;
 
     // TMA of the state-n window of population l that phase 1 of iteration k
     // pulls (column c1(k) - cx_l, rows from ya + A0(l)); one thread per
@@ -403,11 +402,11 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
           const uint32_t kb = kglob + (uint32_t)t;
           const int buf = (int)(kb % NB);
           mbar_wait(smem_u32(bars + buf), (kb / NB) & 1);
-          // the warps that pull across a wall fill the virtual rows themselves
-          // (redundantly if two do: same values) before reading them
+          // wall strips: warp 0 fills the virtual rows (one copy per lane),
+          // then the phase-1 warps meet at named barrier 1 before reading
           if (vbottom || vtop) {
             const int lane = tid & 31;
-            if (lane < NVROW) {
+            if (warp == 0 && lane < NVROW) {
               double* sb = s0 + buf * P0 - ya;
               if (vbottom) {
                 const int2 e = c_vrows.bot[lane];
@@ -418,7 +417,7 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
                 sb[ly + e.x] = sb[ly + e.y];
               }
             }
-            __syncwarp();
+            asm volatile("bar.sync 1, %0;" ::"r"(32 * C::NW1) : "memory");
           }
           const int i = tid;
           const int y = ya - 3 + i;

@@ -26,6 +26,21 @@ for bc in ("thermal", "adiabatic", "periodic"):
             g.exchange()
             g.peek(0)
             g.close()
+# two-step kernel (temporal blocking): several strips incl. moved ones, both
+# walls, monitors on and off, a small grid (several sweeps per CTA)
+for (lx2, ly2), grid in (((40, 250), 0), ((24, 30), 0), ((17, 131), 3)):
+    f2 = lbgen.rt_macro(lx2, ly2, T0)
+    for coll in ("bgk", "regularized"):
+        g = lb.Lattice(lx2, ly2, collision=coll, gravity=(1e-6, -1e-5))
+        g.temporal(True, grid=grid)
+        g.init_macro(*f2)
+        g.step(2)
+        g.monitor(True)
+        g.step(2)
+        buf = np.zeros(10)
+        g.invariants_pair_async(buf)
+        g.invariants()
+        g.close()
 # NCCL 1-rank ring with the overlapped schedule
 g = lb.Lattice(lx, ly, overlap=True, nccl_id=lb.nccl_unique_id())
 g.init_macro(*fields)
