@@ -266,7 +266,8 @@ __device__ __forceinline__ void phase2(const double* s1, double* __restrict__ B,
   if (COLL == COLL_REGULARIZED) collide_site_reg(f, r);
   else collide_site(f, r);
   if (MON && own) acc_invariants(f, acc);
-  const int nyp = opaque(g.nyp);
+  // 64-bit stride: one IMAD.WIDE per store instead of IMAD + LEA + LEA.HI.X
+  const int64_t nyp = opaque(g.nyp);
   double* p = B + (int64_t)c2 * g.cs + g.y0 + y;
 #pragma unroll
   for (int l = 0; l < Q; ++l) p[l * nyp] = f[l];
