@@ -21,7 +21,7 @@ for r in rows:
     if not hdr or len(r) < len(hdr):
         continue
     d = dict(zip(hdr, r))
-    name = d["Kernel Name"].replace("(anonymous namespace)::", "").split("(")[0].replace("void ", "")
+    name = d["Kernel Name"].replace("(anonymous namespace)::", "").replace("unnamed>::", "").split("(")[0].replace("void ", "")
     base = name.split("<")[0]
     targs = name[len(base):].strip("<>").replace(" ", "").split(",") if "<" in name else []
     # collision kind: k_step_fused<BC, COLL, MON> / k_collide<COLL>
