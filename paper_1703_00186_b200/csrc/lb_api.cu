@@ -148,6 +148,7 @@ struct lb_ctx {
   int tb_grid = 0;              // LB_OPT_TB_GRID: CTAs of the two-step kernel (0 = SM count)
   int tb_l2 = 0;                // LB_OPT_TB_L2_PREFETCH: L2 prefetch distance in columns
   int tb_wall_w16 = 20;         // LB_OPT_TB_WALL_WEIGHT: wall-strip column cost x16 (work split)
+  double* d_stage = nullptr;    // N > 1 two-step: the neighbours' 6 edge columns (2 x 6 x cs doubles)
   double* d_mon_tb = nullptr;   // two-step monitors: 2 x cap x 5 per-CTA partials, then reduce scratch
   int mon_tb_cap = 0;           // CTAs d_mon_tb holds partials for
   int mon_tb_G = 0;             // CTAs of the last two-step launch
@@ -352,7 +353,13 @@ int step_peer(lb_ctx* c) {
   const lb_peers& P = c->peers;
   if (!c->halo_fresh)
     TRY(launch(c, "k_peer_pull", c->s, 6LL * c->g.ly, [&] {
-      return lbk::launch_peer_pull(c->g, c->A, P.left_buf[c->par], P.right_buf[c->par], c->s);
+      lbk::Halo w;  // wait for the neighbours' previous launch (it may be a two-step one)
+      w.waitL = reinterpret_cast<const unsigned long long*>(P.left_done);
+      w.waitR = reinterpret_cast<const unsigned long long*>(P.right_done);
+      w.my_done = reinterpret_cast<const unsigned long long*>(P.my_done);
+      w.status = c->d_status;
+      w.timeout_ns = c->peer_timeout_ns;
+      return lbk::launch_peer_pull(c->g, c->A, P.left_buf[c->par], P.right_buf[c->par], w, c->s);
     }));
   lbk::Halo h;
   h.dstL = P.left_buf[c->par ^ 1];
@@ -579,7 +586,8 @@ int lb_init(const lb_params* p, const lb_dist* d, double* f_a, double* f_b, void
   // Two steps per pass (lb_tb.cu) is the default where it applies (N = 1,
   // walls, fused mode; lb_step falls back to one fused step otherwise): it is
   // bit-identical to two fused steps and 1.35x faster at 1920x2048.
-  if (nranks == 1 && p->bc_y != LB_PERIODIC && p->mode == LB_MODE_FUSED) {
+  // (N > 1: once lb_set_peers provides the neighbours' buffers for the staging)
+  if (p->bc_y != LB_PERIODIC && p->mode == LB_MODE_FUSED) {
     c->tb = lbk::tb_create(c->g, c->A, c->B);
     c->tb_on = c->tb != nullptr;
   }
@@ -611,6 +619,7 @@ void lb_destroy(lb_ctx* c) {
   if (c->d_part) cudaFree(c->d_part);
   if (c->d_mon) cudaFree(c->d_mon);
   if (c->d_mon_tb) cudaFree(c->d_mon_tb);
+  if (c->d_stage) cudaFree(c->d_stage);
   if (c->d_ticket) cudaFree(c->d_ticket);
   if (c->d_status) cudaFree(c->d_status);
   if (c->tma) lbk::tma_destroy(c->tma);
@@ -800,8 +809,10 @@ static int graph_two_steps(lb_ctx* c) {
 // Two steps in one pass (lb_tb.cu): N = 1 without NCCL or peers, walls, fused
 // mode, monitors off.  Bit-identical to two fused steps.
 static bool tb_usable(const lb_ctx* c) {
-  return c->tb_on && c->tb && c->nranks == 1 && !c->comm && !c->peers_on && c->p.mode == LB_MODE_FUSED &&
-         c->p.bc_y != LB_PERIODIC && lbk::tb_layout_ok(c->g.ly);
+  const bool alone = c->nranks == 1 && !c->comm && !c->peers_on;  // N = 1 periodic wrap
+  const bool staged = c->peers_on && c->tb && c->tb->staged;       // N > 1 peer mode
+  return c->tb_on && c->tb && (alone || staged) && c->p.mode == LB_MODE_FUSED && c->p.bc_y != LB_PERIODIC &&
+         lbk::tb_layout_ok(c->g.ly);
 }
 
 static int step_tb(lb_ctx* c) {
@@ -816,12 +827,30 @@ static int step_tb(lb_ctx* c) {
     c->mon_tb_cap = G;
   }
   double* mon = c->mon_on ? c->d_mon_tb : nullptr;
+  const lb_peers& P = c->peers;
+  const bool peers = c->peers_on;
+  if (peers)  // N > 1: wait for both neighbours' previous launch, copy their 6 edge columns
+    TRY(launch(c, "k_tb_pull", c->s, 12LL * c->g.ly, [&] {
+      return lbk::launch_tb_pull(c->g, c->d_stage, P.left_buf[c->par], P.right_buf[c->par],
+                                 reinterpret_cast<const unsigned long long*>(P.left_done),
+                                 reinterpret_cast<const unsigned long long*>(P.right_done),
+                                 reinterpret_cast<const unsigned long long*>(P.my_done), c->d_status,
+                                 c->peer_timeout_ns, c->s);
+    }));
   TRY(launch(c, c->p.collision ? "k_step2_tb_reg" : "k_step2_tb", c->s, 2 * c->L.sites, [&] {
     return lbk::launch_step2_tb(c->g, c->tb, c->par, c->B, c->p.bc_y, c->p.collision, c->relax, grid, c->tb_l2,
-                                c->tb_wall_w16, mon, c->s);
+                                c->tb_wall_w16, mon, peers ? 1 : 0, c->s);
   }));
+  if (peers) {  // publish: this launch is complete (the neighbours may now read our new state)
+    c->peer_step += 1;
+    TRY(launch(c, "k_signal", c->s, 0, [&] {
+      return lbk::launch_signal(reinterpret_cast<unsigned long long*>(P.my_done), c->s);
+    }));
+  }
   swap_ab(c);  // B held state n + 2: it becomes A
-  c->halo_fresh = true;  // the kernel stored the border columns into B's halo
+  // N = 1: the kernel stored the border columns into B's halo; N > 1: halos
+  // are not maintained by the two-step path (a following one-step pulls them)
+  c->halo_fresh = !peers;
   fused_step_done(c);
   c->mon_tb = c->mon_on;
   c->mon_tb_G = G;
@@ -1033,6 +1062,12 @@ int lb_set_peers(lb_ctx* c, const lb_peers* p) {
     return fail(LB_ENOMEM, "status allocation failed");
   CU(cudaMemsetAsync(c->d_status, 0, sizeof(unsigned int), c->s));
   if (const char* e = std::getenv("LB_PEER_TIMEOUT_MS")) c->peer_timeout_ns = 1000000ull * std::strtoull(e, nullptr, 10);
+  // two-step kernel at N > 1: staging for the neighbours' edge columns
+  if (c->tb && !c->tb->staged) {
+    if (!c->d_stage && cudaMalloc(&c->d_stage, (size_t)12 * c->g.cs * sizeof(double)) != cudaSuccess)
+      return fail(LB_ENOMEM, "staging allocation failed");
+    if (!lbk::tb_attach_staging(c->tb, c->g, c->d_stage)) return fail(LB_ECUDA, "staging tensor maps failed");
+  }
   c->peers = *p;
   c->peers_on = true;
   c->peer_step = 0;

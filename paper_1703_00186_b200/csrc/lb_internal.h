@@ -84,8 +84,21 @@ cudaError_t launch_step_fused_tma(const Geo& g, const TmaMaps* t, int src_buf, c
 struct TbMaps {
   CUtensorMap load[2];  // per-population windows, box {HT + 8, 1, 1}
   CUtensorMap pf[2];    // L2 prefetch of a column window, box {HT + 16, 37, 1}
+  CUtensorMap st[2];    // N > 1: staging of the left / right neighbour's 6 edge columns
+  bool staged = false;  // st[] encoded (tb_attach_staging)
 };
 TbMaps* tb_create(const Geo& g, double* buf0, double* buf1);
+// N > 1 (peer mode): stage = 2 x 6 x g.cs doubles — [0, 6 cs) the left
+// neighbour's last 6 physical columns (our internal columns -3..2), [6 cs,
+// 12 cs) the right neighbour's first 6 (our internal lx+3..lx+8)
+bool tb_attach_staging(TbMaps* t, const Geo& g, double* stage);
+// Fill the staging buffer from the neighbours' current buffers (peer memory)
+// once both have completed as many launches as this rank (*waitL/R >= *my_done;
+// watchdog: *status = 1 after timeout_ns, 0 = wait forever).
+cudaError_t launch_tb_pull(const Geo& g, double* stage, const double* left_A, const double* right_A,
+                           const unsigned long long* waitL, const unsigned long long* waitR,
+                           const unsigned long long* my_done, unsigned int* status, unsigned long long timeout_ns,
+                           cudaStream_t s);
 // false for the few heights with no valid strip layout (HT < ly < HT + 6)
 bool tb_layout_ok(int ly);
 void tb_destroy(TbMaps* t);
@@ -95,14 +108,19 @@ cudaError_t tb_upload_constants(const double* k_bottom, const double* k_top, con
 // wall_w16: cost of a wall-strip column in 1/16 of an interior one (work split);
 // mon != nullptr: monitors, 2 x tb_grid(g, grid) x 5 doubles of per-CTA
 // partials (state n+1, then state n+2)
+// peers != 0: columns beyond the slab come from the staging buffer (N > 1) and
+// B's halo is not written; else the N = 1 periodic wrap.
 cudaError_t launch_step2_tb(const Geo& g, const TbMaps* t, int src_buf, double* B, int bc, int coll,
-                            const lbd::Relax& r, int grid, int l2_dist, int wall_w16, double* mon, cudaStream_t s);
+                            const lbd::Relax& r, int grid, int l2_dist, int wall_w16, double* mon, int peers,
+                            cudaStream_t s);
 // CTAs a two-step launch with `grid` requested actually uses
 int tb_grid(const Geo& g, int grid);
 // this rank's counter += 1 (system-scope release), after the step kernel
 cudaError_t launch_signal(unsigned long long* done, cudaStream_t s);
+// wait.waitL != nullptr: first wait (watchdog) for both neighbours' counters
+// to reach *wait.my_done (the pull after a two-step launch)
 cudaError_t launch_peer_pull(const Geo& g, double* A, const double* left_A, const double* right_A,
-                             cudaStream_t s);
+                             const Halo& wait, cudaStream_t s);
 cudaError_t launch_init_macro(const Geo& g, double* A, const double* rho, const double* ux,
                               const double* uy, const double* T, cudaStream_t s);
 cudaError_t launch_init_rt(const Geo& g, double* A, const double* eps, int lx_total, int x0, double t_ref,

@@ -434,7 +434,24 @@ cudaError_t launch_signal(unsigned long long* done, cudaStream_t s) {
 // <- right's A[3, 6) (full columns; the caller guarantees the neighbours'
 // states are set and that no step is in flight).
 __global__ void k_peer_pull(double2* __restrict__ A, const double2* L, const double2* R, int64_t lx,
-                            int64_t cs2) {
+                            int64_t cs2, Halo h) {
+  // h.waitL != nullptr: first wait until both neighbours completed as many
+  // launches as this rank (a pull right after a two-step launch: they may
+  // still be writing the state we read), with the watchdog of the step kernel
+  if (h.waitL) {
+    if (threadIdx.x == 0) {
+      const unsigned long long t0 = globaltimer_ns();
+      const unsigned long long want = *h.my_done;
+      while (ld_acquire_sys(h.waitL) < want || ld_acquire_sys(h.waitR) < want) {
+        __nanosleep(128);
+        if (h.timeout_ns && globaltimer_ns() - t0 > h.timeout_ns) {
+          atomicExch(h.status, 1u);
+          break;
+        }
+      }
+    }
+    __syncthreads();
+  }
   const int64_t n = 3 * cs2;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 2 * n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -446,11 +463,11 @@ __global__ void k_peer_pull(double2* __restrict__ A, const double2* L, const dou
 }
 
 cudaError_t launch_peer_pull(const Geo& g, double* A, const double* left_A, const double* right_A,
-                             cudaStream_t s) {
+                             const Halo& wait, cudaStream_t s) {
   const int64_t cs2 = g.cs / 2;
   int blocks = (int)std::min<int64_t>((6 * cs2 + 255) / 256, 148 * 8);
   k_peer_pull<<<blocks, 256, 0, s>>>(reinterpret_cast<double2*>(A), reinterpret_cast<const double2*>(left_A),
-                                     reinterpret_cast<const double2*>(right_A), g.lx, cs2);
+                                     reinterpret_cast<const double2*>(right_A), g.lx, cs2, wait);
   return cudaGetLastError();
 }
 

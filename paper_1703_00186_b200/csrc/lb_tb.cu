@@ -256,7 +256,8 @@ __device__ __forceinline__ void phase1(const double* s0, double* s1, int b, int 
 // state-(n+1) ring, stored to B (+ B's halo for the 3+3 border columns).
 template <int COLL, int R1, bool MON>
 __device__ __forceinline__ void phase2(const double* s1, double* __restrict__ B, const Geo& g, int t, int i,
-                                       int y, int c2, bool thermal, const Relax& r, bool own, double (&acc)[5]) {
+                                       int y, int c2, bool thermal, const Relax& r, bool own, double (&acc)[5],
+                                       bool wrap) {
   const int ly = g.ly;
   double f[Q];
   const int io = opaque(i);
@@ -272,12 +273,12 @@ __device__ __forceinline__ void phase2(const double* s1, double* __restrict__ B,
 #pragma unroll
   for (int l = 0; l < Q; ++l) p[l * nyp] = f[l];
   // N = 1 wrap of the next step: border columns also go to the halo
-  if (c2 < 2 * H) {
+  if (wrap && c2 < 2 * H) {
     double* q = p + (int64_t)g.lx * g.cs;
 #pragma unroll
     for (int l = 0; l < Q; ++l) q[l * nyp] = f[l];
   }
-  if (c2 >= g.lx) {
+  if (wrap && c2 >= g.lx) {
     double* q = p - (int64_t)g.lx * g.cs;
 #pragma unroll
     for (int l = 0; l < Q; ++l) q[l * nyp] = f[l];
@@ -299,7 +300,8 @@ template <int COLL, int HT, int PF, bool MON>
 __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
     k_step2_tb(const __grid_constant__ CUtensorMap src, const __grid_constant__ CUtensorMap pf_map,
                double* __restrict__ B, Geo g, Relax r, int nstrips, int l2_dist, int thermal, int wall_w16,
-               double* __restrict__ mon) {
+               double* __restrict__ mon, const __grid_constant__ CUtensorMap stL,
+               const __grid_constant__ CUtensorMap stR, int peers) {
   using C = TbCfg<HT, PF>;
   constexpr int R0 = C::R0, P0 = C::P0, R1 = C::R1, NB = C::NB;
   extern __shared__ __align__(128) double sm[];
@@ -380,10 +382,18 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
       }
       const int2 pc = c_tb_pop[l];  // (cx_l, A0(l))
       const double* dst = s0 + (l * NB + buf) * P0;
+      // source column: N = 1 periodic wrap; N > 1 the staging buffers beyond
+      // the slab (left: internal -3..2, right: lx+3..lx+8)
+      const int j = c1 - pc.x;
+      const CUtensorMap* m = &src;
+      int col = j;
+      if (!peers) col = wrap_col(j, lx);
+      else if (j < H) { m = &stL; col = j + H; }
+      else if (j >= lx + H) { m = &stR; col = j - lx - H; }
       asm volatile(
           "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
           " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
-          "l"(&src), "r"(rbase + pc.y), "r"(l), "r"(wrap_col(c1 - pc.x, lx)), "r"(bar)
+          "l"(m), "r"(rbase + pc.y), "r"(l), "r"(col), "r"(bar)
           : "memory");
     };
     // lanes [0, 5) of warp w issue populations 5 w + lane (8 warps cover 37)
@@ -431,7 +441,8 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
         const int i = tid - 32 * C::NW1;
         const int y = ya + i;
         if (i < HT && y < ly)
-          phase2<COLL, R1, MON>(s1, B, g, t, i, y, xs - 7 + t, thermal, r, y >= own_lo && y < own_hi, acc);
+          phase2<COLL, R1, MON>(s1, B, g, t, i, y, xs - 7 + t, thermal, r, y >= own_lo && y < own_hi, acc,
+                                !peers);
       }
     }
     kglob += (uint32_t)nload;
@@ -492,7 +503,7 @@ bool encode(CUtensorMap* m, double* base, const Geo& g, int box_rows, int box_po
 
 template <int COLL, bool MON>
 cudaError_t launch_tb(const Geo& g, const TbMaps* t, int src_buf, double* B, const Relax& r, int grid,
-                      int l2_dist, int thermal, int wall_w16, double* mon, cudaStream_t s) {
+                      int l2_dist, int thermal, int wall_w16, double* mon, int peers, cudaStream_t s) {
   auto kern = k_step2_tb<COLL, TB_HT, TB_PF, MON>;
   static unsigned long long done_mask = 0;  // opt-in smem is a per-device attribute
   int dev = 0;
@@ -503,8 +514,12 @@ cudaError_t launch_tb(const Geo& g, const TbMaps* t, int src_buf, double* B, con
     if (e != cudaSuccess) return e;
     if (dev < 64) done_mask |= 1ull << dev;
   }
+  if (peers && !t->staged) return cudaErrorInvalidValue;
+  const CUtensorMap& stl = peers ? t->st[0] : t->load[src_buf];
+  const CUtensorMap& str = peers ? t->st[1] : t->load[src_buf];
   kern<<<tb_grid(g, grid), Cfg::NT, Cfg::SMEM, s>>>(t->load[src_buf], t->pf[src_buf], B, g, r,
-                                                    (g.ly + TB_HT - 1) / TB_HT, l2_dist, thermal, wall_w16, mon);
+                                                    (g.ly + TB_HT - 1) / TB_HT, l2_dist, thermal, wall_w16, mon,
+                                                    stl, str, peers);
   return cudaGetLastError();
 }
 
@@ -542,16 +557,76 @@ cudaError_t tb_upload_constants(const double* k_bottom, const double* k_top, con
 }
 
 cudaError_t launch_step2_tb(const Geo& g, const TbMaps* t, int src_buf, double* B, int bc, int coll,
-                            const Relax& r, int grid, int l2_dist, int wall_w16, double* mon, cudaStream_t s) {
+                            const Relax& r, int grid, int l2_dist, int wall_w16, double* mon, int peers,
+                            cudaStream_t s) {
   if (bc != BC_THERMAL && bc != BC_ADIABATIC) return cudaErrorNotSupported;
   const int th = bc == BC_THERMAL;
   if (mon)
     return coll == COLL_REGULARIZED
-               ? launch_tb<COLL_REGULARIZED, true>(g, t, src_buf, B, r, grid, l2_dist, th, wall_w16, mon, s)
-               : launch_tb<COLL_BGK, true>(g, t, src_buf, B, r, grid, l2_dist, th, wall_w16, mon, s);
+               ? launch_tb<COLL_REGULARIZED, true>(g, t, src_buf, B, r, grid, l2_dist, th, wall_w16, mon, peers, s)
+               : launch_tb<COLL_BGK, true>(g, t, src_buf, B, r, grid, l2_dist, th, wall_w16, mon, peers, s);
   return coll == COLL_REGULARIZED
-             ? launch_tb<COLL_REGULARIZED, false>(g, t, src_buf, B, r, grid, l2_dist, th, wall_w16, mon, s)
-             : launch_tb<COLL_BGK, false>(g, t, src_buf, B, r, grid, l2_dist, th, wall_w16, mon, s);
+             ? launch_tb<COLL_REGULARIZED, false>(g, t, src_buf, B, r, grid, l2_dist, th, wall_w16, mon, peers, s)
+             : launch_tb<COLL_BGK, false>(g, t, src_buf, B, r, grid, l2_dist, th, wall_w16, mon, peers, s);
+}
+
+// ---- N > 1: staging of the neighbours' edge columns (peer memory -> local)
+namespace {
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Every block's thread 0 waits until both neighbours completed as many launches
+// as this rank (their current buffer then holds the same state as ours, and
+// they are done reading our previous one), then the grid copies the left
+// neighbour's internal columns [lx-3, lx+3) and the right one's [3, 9).
+__global__ void __launch_bounds__(256) k_tb_pull(double2* __restrict__ stage, const double2* L, const double2* R,
+                                                 int64_t lx, int64_t cs2, const unsigned long long* waitL,
+                                                 const unsigned long long* waitR, const unsigned long long* my_done,
+                                                 unsigned int* status, unsigned long long timeout_ns) {
+  if (threadIdx.x == 0) {
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    const unsigned long long want = *my_done;
+    while (ld_acquire_sys_u64(waitL) < want || ld_acquire_sys_u64(waitR) < want) {
+      __nanosleep(128);
+      unsigned long long t1;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+      if (timeout_ns && t1 - t0 > timeout_ns) {
+        atomicExch(status, 1u);
+        break;
+      }
+    }
+  }
+  __syncthreads();
+  const int64_t n = 6 * cs2;  // double2 per side
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 2 * n; i += (int64_t)gridDim.x * blockDim.x)
+    stage[i] = i < n ? __ldcg(L + (lx - 3) * cs2 + i) : __ldcg(R + 3 * cs2 + (i - n));
+}
+
+}  // namespace
+
+bool tb_attach_staging(TbMaps* t, const Geo& g, double* stage) {
+  Geo g6 = g;
+  g6.nx = 6;  // 6 columns per side
+  if (!encode(&t->st[0], stage, g6, Cfg::R0, 1) || !encode(&t->st[1], stage + 6 * g.cs, g6, Cfg::R0, 1)) return false;
+  t->staged = true;
+  return true;
+}
+
+cudaError_t launch_tb_pull(const Geo& g, double* stage, const double* left_A, const double* right_A,
+                           const unsigned long long* waitL, const unsigned long long* waitR,
+                           const unsigned long long* my_done, unsigned int* status, unsigned long long timeout_ns,
+                           cudaStream_t s) {
+  const int64_t cs2 = g.cs / 2;
+  const int blocks = (int)std::min<int64_t>((12 * cs2 + 255) / 256, 148 * 4);
+  k_tb_pull<<<blocks, 256, 0, s>>>(reinterpret_cast<double2*>(stage), reinterpret_cast<const double2*>(left_A),
+                                   reinterpret_cast<const double2*>(right_A), g.lx, cs2, waitL, waitR, my_done,
+                                   status, timeout_ns);
+  return cudaGetLastError();
 }
 
 }  // namespace lbk

@@ -46,17 +46,20 @@ def test_sampled_columns_full_size(lb, lx, ly, coll):
     g.close()
 
 
-def test_peer_watchdog_reports_dead_neighbour(lb, monkeypatch):
-    """A rank whose neighbour never steps must not hang: the border blocks give
-    up after LB_PEER_TIMEOUT_MS and lb_sync returns LB_EPEER."""
+@pytest.mark.parametrize("temporal", [False, True])
+def test_peer_watchdog_reports_dead_neighbour(lb, monkeypatch, temporal):
+    """A rank whose neighbour never steps must not hang: the waiting blocks
+    (one-step: the border blocks; two-step: k_tb_pull) give up after
+    LB_PEER_TIMEOUT_MS and lb_sync returns LB_EPEER."""
     monkeypatch.setenv("LB_PEER_TIMEOUT_MS", "200")
     lx, ly = 16, 40
-    r = [lb.Lattice(2 * lx, ly, rank=k, nranks=2) for k in range(2)]
+    r = [lb.Lattice(2 * lx, ly, rank=k, nranks=2, temporal=temporal) for k in range(2)]
     for k, x in enumerate(r):
         x.init_macro(*lbgen.rt_macro(2 * lx, ly, lb.t0(), x0=k * lx, lx=lx))
     r[0].set_peers(r[1], r[1])
     r[1].set_peers(r[0], r[0])
-    r[0].step(2)          # needs r[1]'s step 1, which never comes
+    # the second launch needs r[1]'s first, which never comes
+    r[0].step(4 if temporal else 2)
     with pytest.raises(lb.LBError) as ei:
         r[0].sync()
     assert ei.value.status == 7

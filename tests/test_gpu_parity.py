@@ -398,6 +398,45 @@ def test_peer_exchange_ring_equals_single_lattice(lb, nranks, streams, coll):
         g.close()
 
 
+@pytest.mark.parametrize("nranks,ly,stride,nsteps", [(2, 70, 2, 9), (3, 150, 2, 6), (4, 230, 2, 7), (2, 40, 3, 9)])
+@pytest.mark.parametrize("coll", ["bgk", "regularized"])
+def test_peer_ring_two_step_kernel(lb, nranks, ly, stride, nsteps, coll):
+    """Two-step kernel at N > 1 (peer mode): each launch first waits for both
+    neighbours' launch counters and copies their 6 edge columns into local
+    staging (k_tb_pull), then the two-step kernel reads columns beyond the slab
+    from there.  Steps in pairs (odd remainders: one-step peer launches, whose
+    halo pull follows a two-step launch) on separate streams == the 1-slab run
+    bit for bit."""
+    lx = 24
+    lx_total = lx * nranks
+    T0 = oracle.t0()
+    ref = lb.Lattice(lx_total, ly, collision=coll, gravity=(1e-6, -1e-5))
+    ref.init_macro(*lbgen.rt_macro(lx_total, ly, T0))
+    ref.step(nsteps)
+    want = ref.gather()
+    ranks = []
+    for r in range(nranks):
+        g = lb.Lattice(lx_total, ly, rank=r, nranks=nranks, stream=torch.cuda.Stream(), collision=coll,
+                       gravity=(1e-6, -1e-5))
+        g.init_macro(*lbgen.rt_macro(lx_total, ly, T0, x0=r * lx, lx=lx))
+        ranks.append(g)
+    for r, g in enumerate(ranks):
+        g.set_peers(ranks[(r - 1) % nranks], ranks[(r + 1) % nranks])
+    torch.cuda.synchronize()
+    done = 0
+    while done < nsteps:
+        k = min(stride, nsteps - done)
+        for g in ranks:
+            g.step(k)
+        done += k
+    for g in ranks:
+        g.sync()
+    got = np.concatenate([g.peek(0) for g in ranks], axis=1)
+    assert np.array_equal(got, want)
+    for g in ranks:
+        g.close()
+
+
 # ------------------------------------------------------------------ body force (NEXT 2)
 
 @pytest.mark.parametrize("mode,coll", [("fused", "bgk"), ("split", "bgk"), ("fused", "regularized")])

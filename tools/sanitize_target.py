@@ -59,4 +59,15 @@ for _ in range(3):
         x.step(1)
 for x in r:
     x.sync()
+# two-step kernel at N > 1: staging pull + two-step launches + a one-step
+# remainder (waiting halo pull), monitors on
+for x in r:
+    x.monitor(True)
+for _ in range(2):
+    for x in r:
+        x.step(2)
+for x in r:
+    x.step(1)
+for x in r:
+    x.sync()
 print("sanitize target done", np.isfinite(r[0].peek(0)).all())
