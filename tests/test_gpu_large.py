@@ -65,3 +65,46 @@ def test_peer_watchdog_reports_dead_neighbour(lb, monkeypatch, temporal):
     assert ei.value.status == 7
     for x in r:
         x.close()
+
+
+def window13(g, x, lx):
+    cols = [(x + d) % lx for d in range(-6, 7)]
+    return np.concatenate([g.peek_cols(c, 1) for c in cols], axis=1)
+
+
+@pytest.mark.parametrize("lx,ly,coll", [(1920, 2048, "bgk"), (8192, 8192, "bgk"), (4096, 8192, "regularized")])
+def test_sampled_columns_full_size_two_step(lb, lx, ly, coll):
+    """The two-step kernel (the default bench path) at BASELINE configs #2, #3
+    (8192x8192, N=1) and #4 (4096x8192 per GPU): after one two-step launch,
+    column x depends only on columns x-6..x+6 of the previous state; the oracle
+    steps that 13-column window twice and its centre must match (edge columns
+    of the periodic wrap, strip boundaries and the middle)."""
+    g = lb.Lattice(lx, ly, collision=coll, temporal=True)
+    g.init_macro(*lbgen.rt_macro(lx, ly, lb.t0()))
+    g.step(2)
+    samples = [0, 1, 2, 5, 6, lx // 2 + 1, lx - 7, lx - 6, lx - 3, lx - 1]
+    wins = {x: window13(g, x, lx) for x in samples}
+    g.step(2)
+    for x in samples:
+        got = g.peek_cols(x, 1)[:, 0, :]
+        o = oracle.Lattice(13, ly, collision=oracle.REGULARIZED if coll == "regularized" else oracle.BGK)
+        o.set_state(wins[x])
+        o.step(2)
+        ref = o.get_state(0)[:, 6, :]
+        err = float(np.max(np.abs(got - ref) / np.abs(ref)))
+        assert err < 1e-12, (x, err)
+    g.close()
+
+
+def test_two_step_equals_one_step_full_size(lb):
+    """At 1920x2048 (config #2) two two-step launches == four one-step launches, bit for bit."""
+    lx, ly = 1920, 2048
+    outs = []
+    for temporal in (False, True):
+        g = lb.Lattice(lx, ly, temporal=temporal)
+        g.init_macro(*lbgen.rt_macro(lx, ly, lb.t0()))
+        g.step(4)
+        outs.append(g.gather())
+        g.close()
+        torch.cuda.empty_cache()
+    assert np.array_equal(outs[0], outs[1])
