@@ -396,10 +396,10 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
           "l"(m), "r"(rbase + pc.y), "r"(l), "r"(col), "r"(bar)
           : "memory");
     };
-    // lanes [0, 5) of warp w issue populations 5 w + lane (8 warps cover 37)
-    const int my_pop = 5 * warp + (tid & 31);
-    const bool issuer = (tid & 31) < 5 && my_pop < Q;
-    static_assert(5 * C::NW >= Q, "not enough issuing lanes");
+    // lanes [0, LPW) of warp w issue populations LPW w + lane (all warps cover 37)
+    constexpr int LPW = (Q + C::NW - 1) / C::NW;
+    const int my_pop = LPW * warp + (tid & 31);
+    const bool issuer = (tid & 31) < LPW && my_pop < Q;
 
     if (issuer)
       for (int k = 0; k < PF && k < nload; ++k) issue_one(k, my_pop);
