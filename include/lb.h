@@ -341,7 +341,12 @@ int lb_set_option(lb_ctx* ctx, int option, int value);
  * into a small per-block array, and lb_invariants after such a step sums
  * those partials (one tiny kernel) instead of re-reading the lattice (296
  * B/site).  Values agree with the full pass to rounding (different summation
- * tree).  Allocates lx*ceil(ly/128)*40 B on first enable. */
+ * tree).  Allocates lx*ceil(ly/128)*40 B on first enable.  The two-step
+ * kernel (LB_OPT_TEMPORAL) reduces both of its states per CTA from the
+ * moments its collisions form (rho, j, sum |c|^2 f of each site before the
+ * collision, which the collision conserves, plus the body-force increments of
+ * reading G7b): equal to the sums over the stored states up to rounding;
+ * lb_invariants_pair_async returns both. */
 int lb_monitor(lb_ctx* ctx, int enable);
 
 /* ---- instrumentation ----------------------------------------------------- */

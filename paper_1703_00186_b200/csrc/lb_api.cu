@@ -1021,11 +1021,9 @@ int lb_invariants_pair_async(lb_ctx* c, double* host_out) {
   double* mapped = host_mapped(host_out);
   double* res = c->d_part + lbk::invariants_scratch(c->g);  // 2 x 5 doubles of device result space
   const int G = c->mon_tb_G;
-  for (int k = 0; k < 2; ++k)
-    TRY(launch(c, "k_monitor_reduce", c->s, 0, [&] {
-      return lbk::launch_monitor_reduce(c->d_mon_tb + (int64_t)k * G * 5, G, c->d_mon_tb + (int64_t)c->mon_tb_cap * 10,
-                                        c->d_ticket, mapped ? mapped + 5 * k : res + 5 * k, c->s);
-    }));
+  TRY(launch(c, "k_monitor_reduce_pair", c->s, 0, [&] {
+    return lbk::launch_monitor_reduce_pair(c->d_mon_tb, G, mapped ? mapped : res, c->s);
+  }));
   if (!mapped) CU(cudaMemcpyAsync(host_out, res, 10 * sizeof(double), cudaMemcpyDeviceToHost, c->s));
   return LB_OK;
 }

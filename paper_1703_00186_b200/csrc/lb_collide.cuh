@@ -40,7 +40,9 @@ LB_HD constexpr double ipow(int c, int p) {
 // M'_a = (1 - omega) M_a(f) + omega rho m_p(ux, T) m_q(uy, T): the raw moments
 // of f blended with the Maxwellian moments that f_eq reproduces exactly
 // (m_k(u, T) = E[(u + sqrt(T) Z)^k], lattice units).
-__device__ __forceinline__ void collide_site_reg(double (&f)[Q], const Relax& r) {
+// mo != nullptr: also hand out rho, j = (M_10, M_01) and e = M_20 + M_02 of the
+// pre-collision f (monitors, lb_tb.cu; ux, uy, T are not filled).
+__device__ __forceinline__ void collide_site_reg(double (&f)[Q], const Relax& r, Macro* mo = nullptr) {
   const double omega = r.omega, one_m_omega = r.one_m_omega;
   // 1. column sums T[cx+3][q] = sum_{l: cx_l = cx} cy_l^q f_l
   double T[7][5];
@@ -89,6 +91,12 @@ __device__ __forceinline__ void collide_site_reg(double (&f)[Q], const Relax& r)
   }
   // 3. macroscopic fields (Eq. 2): rho, u, T = (e/rho - |u|^2)/2
   const double rho = M[0];
+  if (mo) {
+    mo->rho = rho;
+    mo->jx = M[6];
+    mo->jy = M[9];
+    mo->e = dadd(M[1], M[2]);
+  }
   const double inv = __drcp_rn(rho);
   const double ux0 = dmul(M[6], inv), uy0 = dmul(M[9], inv);
   const double Tm0 = dmul(0.5, dsub(dmul(dadd(M[1], M[2]), inv), dfma(ux0, ux0, dmul(uy0, uy0))));

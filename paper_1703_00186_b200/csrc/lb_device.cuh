@@ -125,6 +125,7 @@ static_assert(CX(18) == 0 && CY(18) == 0, "rest population");
 
 struct Macro {
   double rho, ux, uy, T;
+  double jx, jy, e;  // the raw sums: j = sum c f, e = sum |c|^2 f
 };
 
 // Relaxation parameters of one launch: omega = dt/tau, 1 - omega, and the
@@ -173,6 +174,9 @@ __device__ __forceinline__ Macro moments(const double (&f)[Q]) {
   const double inv = __drcp_rn(rho);
   Macro m;
   m.rho = rho;
+  m.jx = jx;
+  m.jy = jy;
+  m.e = e;
   m.ux = dmul(jx, inv);
   m.uy = dmul(jy, inv);
   const double uu = dfma(m.ux, m.ux, dmul(m.uy, m.uy));
@@ -210,10 +214,12 @@ __device__ __forceinline__ double cu_of(int l, double Ux, double Uy) {
   return dfma((double)CX(l), Ux, dmul((double)CY(l), Uy));
 }
 
-// f <- f - omega (f - f_eq(moments of f)), in registers.
-__device__ __forceinline__ void collide_site(double (&f)[Q], const Relax& r) {
+// f <- f - omega (f - f_eq(moments of f)), in registers.  mo != nullptr:
+// also hand out the moments of the pre-collision f (monitors, lb_tb.cu).
+__device__ __forceinline__ void collide_site(double (&f)[Q], const Relax& r, Macro* mo = nullptr) {
   const double omega = r.omega, one_m_omega = r.one_m_omega;
   const Macro m = moments(f);
+  if (mo) *mo = m;
   const double ux = dadd(m.ux, r.tgx), uy = dadd(m.uy, r.tgy), Te = dadd(m.T, r.dT);
   const double Ux = dmul(A2, ux), Uy = dmul(A2, uy);
   const double u2 = dmul(A2, dfma(ux, ux, dmul(uy, uy)));

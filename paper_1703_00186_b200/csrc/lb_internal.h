@@ -66,6 +66,8 @@ size_t monitor_slots(const Geo& g);
 constexpr int MON_REDUCE_MAX_BLOCKS = 148;
 cudaError_t launch_monitor_reduce(const double* mon, int64_t nslots, double* part, unsigned int* ticket,
                                   double* out, cudaStream_t s);
+// Two slot sets (nslots each, consecutive) reduced by one block into out[10].
+cudaError_t launch_monitor_reduce_pair(const double* mon, int64_t nslots, double* out, cudaStream_t s);
 // TMA-staged kernels (lb_tma.cu): tensor maps of both buffers, built once.
 // Buffer k viewed as {nyp rows, 37 populations, nx columns}, box {256, 1, 1}.
 struct TmaMaps {

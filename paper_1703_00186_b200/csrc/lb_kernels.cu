@@ -673,6 +673,34 @@ __global__ void __launch_bounds__(RED_TPB) k_monitor_reduce(const double* __rest
   }
 }
 
+// Both states of a two-step launch in ONE single-block launch (nslots per
+// set, set 1 at mon + 5 nslots): out[0..4] = set 0, out[5..9] = set 1.
+__global__ void __launch_bounds__(RED_TPB) k_monitor_reduce_pair(const double* __restrict__ mon, int nslots,
+                                                                 double* out) {
+  __shared__ double sm[5 * RED_TPB];
+  const int t = threadIdx.x;
+  for (int set = 0; set < 2; ++set) {
+    const double* m0 = mon + (int64_t)set * nslots * 5;
+    double v[5] = {0.0, 0.0, 0.0, 0.0, INFINITY};
+    for (int b = t; b < nslots; b += RED_TPB) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) v[k] += m0[(int64_t)b * 5 + k];
+      const double m = m0[(int64_t)b * 5 + 4];
+      v[4] = (m != m || m == -INFINITY) ? -INFINITY : fmin(v[4], m);
+    }
+    block_reduce5(v, sm);
+    if (t == 0)
+#pragma unroll
+      for (int k = 0; k < 5; ++k) out[set * 5 + k] = v[k];
+    __syncthreads();  // sm reused
+  }
+}
+
+cudaError_t launch_monitor_reduce_pair(const double* mon, int64_t nslots, double* out, cudaStream_t s) {
+  k_monitor_reduce_pair<<<1, RED_TPB, 0, s>>>(mon, (int)nslots, out);
+  return cudaGetLastError();
+}
+
 static int monitor_reduce_blocks(int64_t nslots) {
   const int64_t b = (nslots + RED_TPB - 1) / RED_TPB;
   return (int)(b < 1 ? 1 : (b > MON_REDUCE_MAX_BLOCKS ? MON_REDUCE_MAX_BLOCKS : b));

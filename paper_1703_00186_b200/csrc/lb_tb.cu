@@ -205,22 +205,26 @@ constexpr bool vrows_ok() {
 }
 
 // Monitors (lb_monitor): per-thread running sums of the invariants of the
-// sites a CTA owns (rho, j_x, j_y, E = 1/2 sum |c|^2 f, and min rho; a NaN
-// density counts as -inf so the minimum flags it).
-__device__ __forceinline__ void acc_invariants(const double (&f)[Q], double (&a)[5]) {
-  double rho = 0.0, jx = 0.0, jy = 0.0, e = 0.0;
-#pragma unroll
-  for (int l = 0; l < Q; ++l) {
-    rho = __dadd_rn(rho, f[l]);
-    jx = __fma_rn((double)CX(l), f[l], jx);
-    jy = __fma_rn((double)CY(l), f[l], jy);
-    e = __fma_rn(0.5 * (double)c2(l), f[l], e);
-  }
-  a[0] = __dadd_rn(a[0], rho);
-  a[1] = __dadd_rn(a[1], jx);
-  a[2] = __dadd_rn(a[2], jy);
-  a[3] = __dadd_rn(a[3], e);
-  a[4] = fmin(a[4], rho != rho ? -INFINITY : rho);
+// sites a CTA owns after the collision: rho, j_x, j_y, E = 1/2 sum |c|^2 f and
+// min rho (a NaN density counts as -inf so the minimum flags it).  They are
+// formed from the moments the collision computes anyway — rho, j, e = sum
+// |c|^2 f of the pre-collision site — which the collision conserves exactly in
+// arithmetic, plus the body-force increments of reading G7b (j += rho omega tg,
+// E += omega (j . tg + rho (|tg|^2 / 2 + dT)), zero without gravity): a few
+// FP64 operations per site instead of a second pass over the 37 values (the
+// two-step kernel is FP64-latency-bound).  They equal the sums over the stored
+// state up to rounding (tests: <= 1e-13 of the mass).
+__device__ __forceinline__ void acc_invariants(const Macro& m, const Relax& r, double (&a)[5]) {
+  const double djx = __dmul_rn(r.omega, __dmul_rn(m.rho, r.tgx));
+  const double djy = __dmul_rn(r.omega, __dmul_rn(m.rho, r.tgy));
+  const double tg2 = __fma_rn(r.tgx, r.tgx, __dmul_rn(r.tgy, r.tgy));
+  const double dE = __dmul_rn(r.omega, __fma_rn(m.jx, r.tgx, __fma_rn(m.jy, r.tgy,
+                                                    __dmul_rn(m.rho, __fma_rn(0.5, tg2, r.dT)))));
+  a[0] = __dadd_rn(a[0], m.rho);
+  a[1] = __dadd_rn(a[1], __dadd_rn(m.jx, djx));
+  a[2] = __dadd_rn(a[2], __dadd_rn(m.jy, djy));
+  a[3] = __dadd_rn(a[3], __fma_rn(0.5, m.e, dE));
+  a[4] = fmin(a[4], m.rho != m.rho ? -INFINITY : m.rho);
 }
 
 // Phase 1 site update: state n+1 at row y = ya - 3 + i from state-n buffer b
@@ -236,11 +240,13 @@ __device__ __forceinline__ void phase1(const double* s0, double* s1, int b, int 
   for (int l = 0; l < Q; ++l) f[l] = sb[l * NB * P0 - 3 - CY(l) - A0(l)];
   const bool wall = y < 3 || y >= ly - 3;
   if (thermal && wall) thermal_wall(f, y < 3 ? 0 : 1);
-  if (COLL == COLL_REGULARIZED) collide_site_reg(f, r);
-  else collide_site(f, r);
+  Macro mm;
+  Macro* mp = (MON && own) ? &mm : nullptr;
+  if (COLL == COLL_REGULARIZED) collide_site_reg(f, r, mp);
+  else collide_site(f, r, mp);
 #pragma unroll
   for (int l = 0; l < Q; ++l) s1[(SLOTS1_BEFORE(l) + (t % L1(l))) * R1 + io] = f[l];
-  if (MON && own) acc_invariants(f, acc);
+  if (MON && own) acc_invariants(mm, r, acc);
   if (wall) {
     // virtual row of refl(l): -1 - y (bottom) or 2 ly - 1 - y (top); ring row
     // index = absolute row - (ya - 3), and i = y - (ya - 3)
@@ -264,9 +270,11 @@ __device__ __forceinline__ void phase2(const double* s1, double* __restrict__ B,
 #pragma unroll
   for (int l = 0; l < Q; ++l) f[l] = s1[((t - 4 - CX(l)) % L1(l)) * R1 + SLOTS1_BEFORE(l) * R1 + io + 3 - CY(l)];
   if (thermal && (y < 3 || y >= ly - 3)) thermal_wall(f, y < 3 ? 0 : 1);
-  if (COLL == COLL_REGULARIZED) collide_site_reg(f, r);
-  else collide_site(f, r);
-  if (MON && own) acc_invariants(f, acc);
+  Macro mm;
+  Macro* mp = (MON && own) ? &mm : nullptr;
+  if (COLL == COLL_REGULARIZED) collide_site_reg(f, r, mp);
+  else collide_site(f, r, mp);
+  if (MON && own) acc_invariants(mm, r, acc);
   // 64-bit stride: one IMAD.WIDE per store instead of IMAD + LEA + LEA.HI.X
   const int64_t nyp = opaque(g.nyp);
   double* p = B + (int64_t)c2 * g.cs + g.y0 + y;

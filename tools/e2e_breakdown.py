@@ -59,6 +59,14 @@ for _ in range(2):
         for k in range(K):
             g.step(1)
     timed("steps_plain_loop_ms", loop_plain)
+    g.monitor(True)
+
+    def pair_steps():   # the two-step kernel with monitors of both states (bench e2e loop)
+        for k in range(0, K, 2):
+            g.step(2)
+            g.invariants_pair_async(mon[k:k + 2])
+    timed("steps_pair_monitored_ms", pair_steps)
+    g.monitor(False)
     timed("gather_ms", lambda: g.gather(out=out.numpy()))
 g.monitor(True)
 g.profile(True)
@@ -67,7 +75,15 @@ for k in range(200):
     g.step(1)
     g.invariants_async(mon[k])
 g.sync()
-res["profile_monitored_200"] = {k: round(v["total_ms"] / v["launches"] * 1e3, 2) for k, v in g.profile_read().items()}
+res["profile_monitored_200"] = {k: round(v["total_ms"] / v["launches"] * 1e3, 2) for k, v in g.profile_read().items()
+                                if v["launches"]}
+g.profile_reset()
+for k in range(0, 200, 2):
+    g.step(2)
+    g.invariants_pair_async(mon[k:k + 2])
+g.sync()
+res["profile_pair_monitored_200"] = {k: round(v["total_ms"] / v["launches"] * 1e3, 2)
+                                     for k, v in g.profile_read().items() if v["launches"]}
 g.profile(False)
 g.monitor(False)
 res["K"] = K
