@@ -324,7 +324,9 @@ int lb_sync(lb_ctx* ctx);
  * fused steps; an odd remainder takes one fused step.  LB_OPT_TB_GRID: CTAs of
  * that kernel (0 = one per SM), LB_OPT_TB_L2_PREFETCH: L2 prefetch distance in
  * columns (0 = off, <= 64).  LB_OPT_TB_WALL_WEIGHT: cost of a column of a
- * wall strip relative to an interior one, x16 (work split; default 20). */
+ * wall strip relative to an interior one, x16 (work split; default 20).
+ * LB_OPT_TB_L2_PROMOTION: L2 promotion of that kernel's TMA window loads in
+ * bytes (0 = none, 64 = default, 128, 256); results do not depend on it. */
 enum lb_option {
   LB_OPT_PROPAGATE_IMPL = 0,
   LB_OPT_FUSED_IMPL = 1,
@@ -332,7 +334,8 @@ enum lb_option {
   LB_OPT_TEMPORAL = 3,
   LB_OPT_TB_GRID = 4,
   LB_OPT_TB_L2_PREFETCH = 5,
-  LB_OPT_TB_WALL_WEIGHT = 6
+  LB_OPT_TB_WALL_WEIGHT = 6,
+  LB_OPT_TB_L2_PROMOTION = 7
 };
 int lb_set_option(lb_ctx* ctx, int option, int value);
 

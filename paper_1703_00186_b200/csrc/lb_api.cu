@@ -147,6 +147,7 @@ struct lb_ctx {
   int tb_on = 0;                // LB_OPT_TEMPORAL: two steps per pass where possible
   int tb_grid = 0;              // LB_OPT_TB_GRID: CTAs of the two-step kernel (0 = SM count)
   int tb_l2 = 0;                // LB_OPT_TB_L2_PREFETCH: L2 prefetch distance in columns
+  int tb_promo = 64;            // LB_OPT_TB_L2_PROMOTION: L2 promotion of its TMA loads (bytes)
   int tb_wall_w16 = 20;         // LB_OPT_TB_WALL_WEIGHT: wall-strip column cost x16 (work split)
   double* d_stage = nullptr;    // N > 1 two-step: the neighbours' 6 edge columns (2 x 6 x cs doubles)
   double* d_mon_tb = nullptr;   // two-step monitors: 2 x cap x 5 per-CTA partials, then reduce scratch
@@ -588,7 +589,7 @@ int lb_init(const lb_params* p, const lb_dist* d, double* f_a, double* f_b, void
   // bit-identical to two fused steps and 1.35x faster at 1920x2048.
   // (N > 1: once lb_set_peers provides the neighbours' buffers for the staging)
   if (p->bc_y != LB_PERIODIC && p->mode == LB_MODE_FUSED) {
-    c->tb = lbk::tb_create(c->g, c->A, c->B);
+    c->tb = lbk::tb_create(c->g, c->A, c->B, c->tb_promo);
     c->tb_on = c->tb != nullptr;
   }
   if (d && d->nccl_id) {
@@ -1094,7 +1095,7 @@ int lb_set_option(lb_ctx* c, int option, int value) {
     case LB_OPT_TEMPORAL:
       if (value != 0 && value != 1) return fail(LB_EINVAL, "temporal blocking must be 0 or 1");
       if (value == 1 && !c->tb) {
-        c->tb = lbk::tb_create(c->g, c->par ? c->B : c->A, c->par ? c->A : c->B);
+        c->tb = lbk::tb_create(c->g, c->par ? c->B : c->A, c->par ? c->A : c->B, c->tb_promo);
         if (!c->tb) return fail(LB_ECUDA, "two-step kernel unavailable (tensor maps or lx < 6)");
       }
       c->tb_on = value;
@@ -1106,6 +1107,12 @@ int lb_set_option(lb_ctx* c, int option, int value) {
     case LB_OPT_TB_L2_PREFETCH:
       if (value < 0 || value > 64) return fail(LB_EINVAL, "L2 prefetch distance must be in [0, 64]");
       c->tb_l2 = value;
+      return LB_OK;
+    case LB_OPT_TB_L2_PROMOTION:
+      if (value != 0 && value != 64 && value != 128 && value != 256)
+        return fail(LB_EINVAL, "L2 promotion must be 0, 64, 128 or 256");
+      c->tb_promo = value;
+      if (c->tb && !lbk::tb_set_promotion(c->tb, c->g, value)) return fail(LB_ECUDA, "tensor-map re-encoding failed");
       return LB_OK;
     case LB_OPT_TB_WALL_WEIGHT:
       if (value < 1 || value > 256) return fail(LB_EINVAL, "wall weight (x16) must be in [1, 256]");

@@ -84,12 +84,17 @@ cudaError_t launch_step_fused_tma(const Geo& g, const TmaMaps* t, int src_buf, c
 // (periodic wrap in the coordinates), so A's halo is not read; B's halo is
 // written (the next step's wrap).
 struct TbMaps {
-  CUtensorMap load[2];  // per-population windows, box {HT + 8, 1, 1}
-  CUtensorMap pf[2];    // L2 prefetch of a column window, box {HT + 16, 37, 1}
-  CUtensorMap st[2];    // N > 1: staging of the left / right neighbour's 6 edge columns
+  CUtensorMap load[2][3];  // column-group windows, box {HT + 12, 3 | 5 | 7, 1}, per buffer
+  CUtensorMap pf[2];       // L2 prefetch of a column window, box {HT + 16, 37, 1}
+  CUtensorMap st[2][3];    // N > 1: staging of the left / right neighbour's 6 edge columns
   bool staged = false;  // st[] encoded (tb_attach_staging)
+  int promo = 0;        // L2 promotion of every map: 0 / 64 / 128 / 256 bytes (LB_OPT_TB_L2_PROMOTION)
+  double* bufs[2] = {nullptr, nullptr};
+  double* stage = nullptr;
 };
-TbMaps* tb_create(const Geo& g, double* buf0, double* buf1);
+TbMaps* tb_create(const Geo& g, double* buf0, double* buf1, int promo);
+// re-encode every map of t with another L2 promotion (0 / 64 / 128 / 256)
+bool tb_set_promotion(TbMaps* t, const Geo& g, int promo);
 // N > 1 (peer mode): stage = 2 x 6 x g.cs doubles — [0, 6 cs) the left
 // neighbour's last 6 physical columns (our internal columns -3..2), [6 cs,
 // 12 cs) the right neighbour's first 6 (our internal lx+3..lx+8)

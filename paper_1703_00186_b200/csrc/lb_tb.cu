@@ -11,13 +11,14 @@
 //
 // Tiling.  A CTA owns a strip of HT rows [ya, ya+HT) and sweeps a range of
 // output columns [xs, xs + W) in x.  Iteration t of a sweep:
-//   * TMA: for every population l, the window of state n that phase 1 of
-//     iteration t + PF pulls it from — column c1(t + PF) - cx_l (wrapped
-//     periodically: N = 1 needs no halo), rows [ya - 3 - cy_l, ya + HT + 3 -
-//     cy_l) rounded out to a 16-byte box start (the TMA alignment rule,
-//     tools/tma_probe.cu), R0 = HT + 8 rows.  The TMA coordinates perform the
-//     whole pull (propagate), so the state-n ring is just PF + 1 buffers per
-//     population.  The 37 loads are issued by the lane 0s of all warps;
+//   * TMA: for every column group g (the populations of one cx_g, consecutive
+//     labels), the window of state n that phase 1 of iteration t + PF pulls
+//     them from — column c1(t + PF) - cx_g (wrapped periodically: N = 1 needs
+//     no halo), rows [ya - 6, ya + HT + 6) (the union over cy of the rows
+//     [ya - 3 - cy, ya + HT + 3 - cy); ya even, so the box starts on 16 bytes,
+//     the TMA alignment rule of tools/tma_probe.cu), RB = HT + 12 rows.  The
+//     TMA coordinates perform the whole x-pull (propagate), so the state-n
+//     ring is just PF + 1 buffers.  7 loads per column, one per issuing lane;
 //   * phase 1 (warps [0, NW1)): state n+1 at column c1 = xs - 3 + t for the
 //     R1 = HT + 6 rows [ya - 3, ya + HT + 3) (the ±3-row apron step n+2 pulls
 //     from), written to the state-(n+1) ring;
@@ -29,7 +30,7 @@
 //
 // State-(n+1) ring.  Population l of column c1 is pulled by phase 2 at column
 // c1 + cx_l, cx_l + 4 iterations later: cx_l + 5 slots of R1 rows (185 slots
-// over the 37 populations).  HT = 104, PF = 1: 66 KB (state n) + 163 KB
+// over the 37 populations).  HT = 104, PF = 1: 69 KB (state n) + 163 KB
 // (state n+1) of shared memory, 214 sites per iteration, 8 warps.
 //
 // Walls (G9) are data: the mirrored populations are copied into ring rows
@@ -53,11 +54,6 @@ using namespace lbd;
 namespace {
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-// relative start row (to ya) of population l's state-n window: -3 - cy_l,
-// lowered by one when that is odd (box starts must be 16-byte aligned; ya and
-// y0 are even)
-LB_HD constexpr int A0(int l) { return -3 - CY(l) - ((CY(l) + 1) & 1); }
 
 LB_HD constexpr int L1(int l) { return CX(l) + 5; }
 
@@ -88,32 +84,57 @@ static_assert(tables_ok(), "CXSUM / REFL tables");
 // state-(n+1) ring slots of the populations before l
 LB_HD constexpr int SLOTS1_BEFORE(int l) { return CXSUM(l) + 5 * l; }
 
-// per-population TMA parameters for the issuing threads: (cx_l, A0(l))
-__constant__ int2 c_tb_pop[Q] = {
-#define LBTB_P(l) {CX(l), A0(l)}
-    LBTB_P(0),  LBTB_P(1),  LBTB_P(2),  LBTB_P(3),  LBTB_P(4),  LBTB_P(5),  LBTB_P(6),  LBTB_P(7),
-    LBTB_P(8),  LBTB_P(9),  LBTB_P(10), LBTB_P(11), LBTB_P(12), LBTB_P(13), LBTB_P(14), LBTB_P(15),
-    LBTB_P(16), LBTB_P(17), LBTB_P(18), LBTB_P(19), LBTB_P(20), LBTB_P(21), LBTB_P(22), LBTB_P(23),
-    LBTB_P(24), LBTB_P(25), LBTB_P(26), LBTB_P(27), LBTB_P(28), LBTB_P(29), LBTB_P(30), LBTB_P(31),
-    LBTB_P(32), LBTB_P(33), LBTB_P(34), LBTB_P(35), LBTB_P(36)};
-#undef LBTB_P
+// Column groups.  The labels run cx = +3 .. -3 with cy ascending (App. A), so
+// the populations of one cx are consecutive labels: group g = 3 - cx holds
+// GN(g) populations from label GFIRST(g).  Phase 1 pulls every population of
+// group g from the same state-n column c1 - cx, and the union of their row
+// windows is [ya - 6, ya + HT + 6), so ONE TMA box {HT + 12 rows, GN(g)
+// populations, 1 column} loads the whole group: 7 TMA loads per column
+// instead of 37.  Box heights of 3, 5 and 7 populations need 3 tensor maps
+// (class GCLS(g)).
+constexpr int NG = 7;
+LB_HD constexpr int GFIRST(int g) {
+  constexpr int t[NG + 1] = {0, 3, 8, 15, 22, 29, 34, 37};
+  return t[g];
+}
+LB_HD constexpr int GN(int g) { return GFIRST(g + 1) - GFIRST(g); }
+LB_HD constexpr int GCLS(int g) { return GN(g) == 3 ? 0 : (GN(g) == 5 ? 1 : 2); }
+LB_HD constexpr int GOF(int l) { return 3 - CX(l); }  // group of population l
+constexpr int CLS_N[3] = {3, 5, 7};
+constexpr bool groups_ok() {
+  for (int l = 0; l < Q; ++l)
+    if (l < GFIRST(GOF(l)) || l >= GFIRST(GOF(l) + 1)) return false;
+  for (int g = 0; g < NG; ++g)
+    if (CLS_N[GCLS(g)] != GN(g)) return false;
+  return true;
+}
+static_assert(groups_ok(), "column groups of the label order");
+// shared-memory offset (doubles) of group g in a state-n buffer: each group's
+// slab starts on a 128-byte boundary (TMA destination alignment)
+LB_HD constexpr int GOFF(int g, int RB) {
+  int o = 0;
+  for (int h = 0; h < g; ++h) o += (GN(h) * RB + 15) / 16 * 16;
+  return o;
+}
+// offset of population l's window (row ya - 6) in a state-n buffer
+LB_HD constexpr int POFF(int l, int RB) { return GOFF(GOF(l), RB) + (l - GFIRST(GOF(l))) * RB; }
 
 template <int HT_, int PF_>
 struct TbCfg {
   static constexpr int HT = HT_;
   static constexpr int PF = PF_;
-  static constexpr int R0 = HT + 8;                 // TMA box rows of a state-n window
-  static constexpr int P0 = (R0 + 15) / 16 * 16;    // buffer pitch: TMA smem destinations are 128-byte aligned
+  static constexpr int RB = HT + 12;                // TMA box rows of a group window [ya - 6, ya + HT + 6)
+  static constexpr int BUFD = GOFF(NG, RB);         // doubles per state-n buffer (7 group slabs)
   static constexpr int R1 = HT + 6;
   static constexpr int NW1 = (R1 + 31) / 32;        // phase-1 warps
   static constexpr int NW2 = (HT + 31) / 32;        // phase-2 warps
   static constexpr int NW = NW1 + NW2;
   static constexpr int NT = 32 * NW;
   static constexpr int NB = PF + 1;                 // state-n buffers per population = mbarriers
-  static constexpr int S0_DBL = Q * NB * P0;
+  static constexpr int S0_DBL = NB * BUFD;
   static constexpr int S1_DBL = SLOTS1_BEFORE(Q) * R1;
   static constexpr size_t SMEM = (size_t)(S0_DBL + S1_DBL) * sizeof(double) + NB * sizeof(uint64_t);
-  static_assert(R0 % 2 == 0 && R0 <= 256, "TMA box rows");
+  static_assert(RB % 2 == 0 && RB <= 256, "TMA box rows");
   static_assert(SMEM <= 232448, "shared memory per CTA");
   static_assert(NW <= 8, "two warps per scheduler at most (64 KB register file per scheduler)");
 };
@@ -172,29 +193,29 @@ LB_HD inline int strip_ya(int s, int nstrips, int ly, int HT) {
 }
 
 // State-n virtual rows.  Buffer b (just arrived): population l's window comes
-// from the same column as refl(l)'s (same cx), so the virtual rows are copies
-// within buffer b — 26 per wall (cy_l > 0: rows -1..-cy_l at the bottom;
-// cy_l < 0: rows ly..ly+|cy_l|-1 at the top), one per lane.  Offsets relative
-// to s0 + b·P0 - ya (bottom) or s0 + b·P0 - ya + ly (top); the strip layout
-// guarantees every copy lies inside its window (strip_ya).
+// from the same column as refl(l)'s (same cx, same group), so the virtual rows
+// are copies within buffer b — 26 per wall (cy_l > 0: rows -1..-cy_l at the
+// bottom; cy_l < 0: rows ly..ly+|cy_l|-1 at the top), one per lane.  Offsets
+// relative to s0 + b·BUFD - ya (bottom) or s0 + b·BUFD - ya + ly (top); the
+// strip layout keeps every copy inside the window [ya - 6, ya + HT + 6): a
+// bottom strip has ya = 0, a top strip ends on the wall (strip_ya).
 constexpr int NVROW = 26;
 struct VRowTab {
   int2 bot[32], top[32];  // (dst, src) offsets; entries >= NVROW unused
 };
-template <int NB, int P0>
+template <int RB>
 constexpr VRowTab make_vrows() {
   VRowTab t{};
   int nb = 0, nt = 0;
   for (int l = 0; l < Q; ++l) {
     const int c = CY(l), m = REFL(l);
     for (int q = 1; q <= c; ++q)  // row -q <- refl row q - 1
-      t.bot[nb++] = int2{l * NB * P0 - A0(l) - q, m * NB * P0 - A0(m) + q - 1};
+      t.bot[nb++] = int2{POFF(l, RB) + 6 - q, POFF(m, RB) + 6 + q - 1};
     for (int q = 0; q < -c; ++q)  // row ly + q <- refl row ly - 1 - q
-      t.top[nt++] = int2{l * NB * P0 - A0(l) + q, m * NB * P0 - A0(m) - 1 - q};
+      t.top[nt++] = int2{POFF(l, RB) + 6 + q, POFF(m, RB) + 6 - 1 - q};
   }
   return t;
 }
-template <int NB, int P0>
 constexpr bool vrows_ok() {
   int nb = 0, nt = 0;
   for (int l = 0; l < Q; ++l) {
@@ -230,14 +251,19 @@ __device__ __forceinline__ void acc_invariants(const Macro& m, const Relax& r, d
 // Phase 1 site update: state n+1 at row y = ya - 3 + i from state-n buffer b
 // (the pulled values), result into the state-(n+1) ring slot of iteration t;
 // the rows next to a wall also write the virtual rows their values mirror into.
-template <int COLL, int NB, int P0, int R1, bool MON>
-__device__ __forceinline__ void phase1(const double* s0, double* s1, int b, int t, int i, int y, int ly,
-                                       bool thermal, const Relax& r, bool own, double (&acc)[5]) {
-  double f[Q];
+// row y = ya - 3 + i of population l pulls row y - cy_l: window index i + 3 - cy_l
+template <int BUFD, int RB>
+__device__ __forceinline__ void phase1_gather(const double* s0, int b, int i, double (&f)[Q]) {
   const int io = opaque(i);  // not hoistable: no per-population address registers
-  const double* sb = s0 + b * P0 + io;
+  const double* sb = s0 + b * BUFD + io;
 #pragma unroll
-  for (int l = 0; l < Q; ++l) f[l] = sb[l * NB * P0 - 3 - CY(l) - A0(l)];
+  for (int l = 0; l < Q; ++l) f[l] = sb[POFF(l, RB) + 3 - CY(l)];
+}
+
+template <int COLL, int R1, bool MON>
+__device__ __forceinline__ void phase1_update(double (&f)[Q], double* s1, int t, int i, int y, int ly,
+                                              bool thermal, const Relax& r, bool own, double (&acc)[5]) {
+  const int io = opaque(i);
   const bool wall = y < 3 || y >= ly - 3;
   if (thermal && wall) thermal_wall(f, y < 3 ? 0 : 1);
   Macro mm;
@@ -260,6 +286,14 @@ __device__ __forceinline__ void phase1(const double* s0, double* s1, int b, int 
 
 // Phase 2 site update: state n+2 at row y = ya + i, column c2, from the
 // state-(n+1) ring, stored to B (+ B's halo for the 3+3 border columns).
+template <int COLL, int BUFD, int RB, int R1, bool MON>
+__device__ __forceinline__ void phase1(const double* s0, double* s1, int b, int t, int i, int y, int ly,
+                                       bool thermal, const Relax& r, bool own, double (&acc)[5]) {
+  double f[Q];
+  phase1_gather<BUFD, RB>(s0, b, i, f);
+  phase1_update<COLL, R1, MON>(f, s1, t, i, y, ly, thermal, r, own, acc);
+}
+
 template <int COLL, int R1, bool MON>
 __device__ __forceinline__ void phase2(const double* s1, double* __restrict__ B, const Geo& g, int t, int i,
                                        int y, int c2, bool thermal, const Relax& r, bool own, double (&acc)[5],
@@ -293,11 +327,30 @@ __device__ __forceinline__ void phase2(const double* s1, double* __restrict__ B,
   }
 }
 
-constexpr int TB_HT = 104;
-constexpr int TB_PF = 1;
+#ifndef LB_TB_HT
+#define LB_TB_HT 104
+#define LB_TB_PF 1
+#endif
+constexpr int TB_HT = LB_TB_HT;
+constexpr int TB_PF = LB_TB_PF;
 using Cfg = TbCfg<TB_HT, TB_PF>;
-static_assert(vrows_ok<Cfg::NB, Cfg::P0>(), "virtual-row copy count");
-__constant__ VRowTab c_vrows = make_vrows<Cfg::NB, Cfg::P0>();
+static_assert(vrows_ok(), "virtual-row copy count");
+__constant__ VRowTab c_vrows = make_vrows<Cfg::RB>();
+static_assert(GOFF(NG, Cfg::RB) == Cfg::BUFD, "group slabs");
+
+// per-group TMA parameters of the issuing threads: (box class, first label,
+// slab offset in a state-n buffer, cx)
+__constant__ int4 c_tb_grp[NG] = {
+#define LBTB_G(g) {GCLS(g), GFIRST(g), GOFF(g, Cfg::RB), 3 - g}
+    LBTB_G(0), LBTB_G(1), LBTB_G(2), LBTB_G(3), LBTB_G(4), LBTB_G(5), LBTB_G(6)};
+#undef LBTB_G
+
+// Kernel tensor maps (all __grid_constant__): the state-n group windows of the
+// source buffer per box class (3 / 5 / 7 populations), the same for the N > 1
+// staging of the left / right neighbour's edge columns, and the L2 prefetch box.
+struct alignas(64) TbKMaps {
+  CUtensorMap src[3], stL[3], stR[3], pf;
+};
 
 // Warps [0, NW1): phase 1; [NW1, NW1 + NW2): phase 2.
 // MON: monitors — each CTA reduces the invariants of the sites it owns (rows
@@ -306,12 +359,13 @@ __constant__ VRowTab c_vrows = make_vrows<Cfg::NB, Cfg::P0>();
 // (5 doubles each; fixed-order reductions, deterministic).
 template <int COLL, int HT, int PF, bool MON>
 __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
-    k_step2_tb(const __grid_constant__ CUtensorMap src, const __grid_constant__ CUtensorMap pf_map,
-               double* __restrict__ B, Geo g, Relax r, int nstrips, int l2_dist, int thermal, int wall_w16,
-               double* __restrict__ mon, const __grid_constant__ CUtensorMap stL,
-               const __grid_constant__ CUtensorMap stR, int peers) {
+    k_step2_tb(const __grid_constant__ TbKMaps km, double* __restrict__ B, Geo g, Relax r, int nstrips,
+               int l2_dist, int thermal, int wall_w16, double* __restrict__ mon, int peers) {
   using C = TbCfg<HT, PF>;
-  constexpr int R0 = C::R0, P0 = C::P0, R1 = C::R1, NB = C::NB;
+  constexpr int RB = C::RB, BUFD = C::BUFD, R1 = C::R1, NB = C::NB;
+  // PF = 0: one state-n buffer, refilled by the phase-1 warps right after they
+  // gathered from it (the TMA then overlaps their collisions)
+  constexpr bool EARLY = PF == 0;
   extern __shared__ __align__(128) double sm[];
   double* s0 = sm;
   double* s1 = sm + C::S0_DBL;
@@ -367,54 +421,56 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
     const bool vbottom = ya - 3 < 3;
     const bool vtop = ya + HT + 3 > ly - 3;
 
-    // TMA of the state-n window of population l that phase 1 of iteration k
-    // pulls (column c1(k) - cx_l, rows from ya + A0(l)); one thread per
-    // population; the thread of l = 0 also posts the expected bytes
-    // (complete_tx may precede it: the phase cannot complete before that
-    // single arrival)
-    auto issue_one = [&](int k, int l) {
+    // TMA of the state-n window of column group g that phase 1 of iteration k
+    // pulls (column c1(k) - cx_g, rows [ya - 6, ya + HT + 6)); one thread per
+    // group; the thread of g = 0 also posts the expected bytes (complete_tx may
+    // precede it: the phase cannot complete before that single arrival)
+    auto issue_one = [&](int k, int gq) {
       const uint32_t kb = kglob + (uint32_t)k;
       const uint32_t bar = smem_u32(bars + kb % NB);
       const int buf = (int)(kb % NB);
       const int c1 = xs - 3 + k;
-      if (l == 0) {
+      if (gq == 0) {
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
-                     "r"((uint32_t)(Q * R0 * sizeof(double))));
+                     "r"((uint32_t)(Q * RB * sizeof(double))));
         if (l2_dist > 0 && k + l2_dist < nload) {
           // the newest column any population of iteration k + l2_dist touches
           const int pcol = wrap_col(c1 + l2_dist + 3, lx);
-          asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(&pf_map),
+          asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(&km.pf),
                        "r"(rbase - 8), "r"(0), "r"(pcol)
                        : "memory");
         }
       }
-      const int2 pc = c_tb_pop[l];  // (cx_l, A0(l))
-      const double* dst = s0 + (l * NB + buf) * P0;
+      const int4 gp = c_tb_grp[gq];  // (box class, first label, slab offset, cx)
+      const int cls = gp.x;
+      const double* dst = s0 + buf * BUFD + gp.z;
       // source column: N = 1 periodic wrap; N > 1 the staging buffers beyond
       // the slab (left: internal -3..2, right: lx+3..lx+8)
-      const int j = c1 - pc.x;
-      const CUtensorMap* m = &src;
+      const int j = c1 - gp.w;
+      const CUtensorMap* m = &km.src[cls];
       int col = j;
       if (!peers) col = wrap_col(j, lx);
-      else if (j < H) { m = &stL; col = j + H; }
-      else if (j >= lx + H) { m = &stR; col = j - lx - H; }
+      else if (j < H) { m = &km.stL[cls]; col = j + H; }
+      else if (j >= lx + H) { m = &km.stR[cls]; col = j - lx - H; }
       asm volatile(
           "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
           " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
-          "l"(m), "r"(rbase + pc.y), "r"(l), "r"(col), "r"(bar)
+          "l"(m), "r"(rbase - 6), "r"(gp.y), "r"(col), "r"(bar)
           : "memory");
     };
-    // lanes [0, LPW) of warp w issue populations LPW w + lane (all warps cover 37)
-    constexpr int LPW = (Q + C::NW - 1) / C::NW;
-    const int my_pop = LPW * warp + (tid & 31);
-    const bool issuer = (tid & 31) < LPW && my_pop < Q;
+    // lanes [0, GPW) of warp w issue groups GPW w + lane (EARLY: the phase-1
+    // warps only — they refill their single buffer right after gathering from it)
+    constexpr int NWI = EARLY ? C::NW1 : (C::NW < NG ? C::NW : NG);
+    constexpr int GPW = (NG + NWI - 1) / NWI;
+    const int my_grp = GPW * warp + (tid & 31);
+    const bool issuer = warp < NWI && (tid & 31) < GPW && my_grp < NG;
 
     if (issuer)
-      for (int k = 0; k < PF && k < nload; ++k) issue_one(k, my_pop);
+      for (int k = 0; k < (EARLY ? 1 : PF) && k < nload; ++k) issue_one(k, my_grp);
 
     for (int t = 0; t < niter; ++t) {
       __syncthreads();  // every read of iteration t-1 is done: the buffers refilled below are free
-      if (issuer && t + PF < nload) issue_one(t + PF, my_pop);
+      if (!EARLY && issuer && t + PF < nload) issue_one(t + PF, my_grp);
       if (warp < C::NW1) {
         if (t < nload) {
           // phase 1: state n+1 at column c1 = xs - 3 + t, rows [ya-3, ya+HT+3)
@@ -426,7 +482,7 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
           if (vbottom || vtop) {
             const int lane = tid & 31;
             if (warp == 0 && lane < NVROW) {
-              double* sb = s0 + buf * P0 - ya;
+              double* sb = s0 + buf * BUFD - ya;
               if (vbottom) {
                 const int2 e = c_vrows.bot[lane];
                 sb[e.x] = sb[e.y];
@@ -435,14 +491,26 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
                 const int2 e = c_vrows.top[lane];
                 sb[ly + e.x] = sb[ly + e.y];
               }
+              // generic-proxy writes to a buffer the TMA (async proxy) refills later
+              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             }
             asm volatile("bar.sync 1, %0;" ::"r"(32 * C::NW1) : "memory");
           }
           const int i = tid;
           const int y = ya - 3 + i;
-          if (i < R1 && y >= 0 && y < ly)
-            phase1<COLL, NB, P0, R1, MON>(s0, s1, buf, t, i, y, ly, thermal, r,
-                                          t >= 3 && t < W + 3 && y >= own_lo && y < own_hi, acc);
+          const bool valid = i < R1 && y >= 0 && y < ly;
+          const bool own = t >= 3 && t < W + 3 && y >= own_lo && y < own_hi;
+          if (EARLY) {
+            // gather, then (all phase-1 warps done reading) refill the buffer
+            // with iteration t + 1's windows while the collisions run
+            double f[Q];
+            phase1_gather<BUFD, RB>(s0, buf, valid ? i : 0, f);
+            asm volatile("bar.sync 2, %0;" ::"r"(32 * C::NW1) : "memory");
+            if (issuer && t + 1 < nload) issue_one(t + 1, my_grp);
+            if (valid) phase1_update<COLL, R1, MON>(f, s1, t, i, y, ly, thermal, r, own, acc);
+          } else if (valid) {
+            phase1<COLL, BUFD, RB, R1, MON>(s0, s1, buf, t, i, y, ly, thermal, r, own, acc);
+          }
         }
       } else if (t >= 7) {
         // phase 2: state n+2 at column c2 = xs - 7 + t, rows [ya, ya+HT)
@@ -486,9 +554,16 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
   }
 }
 
-// TMA maps of one buffer: per-population windows (box {R0, 1, 1}) and the
+// TMA maps of one buffer: group windows (box {HT + 12, 3 | 5 | 7, 1}) and the
 // whole-column L2 prefetch box {HT + 16, 37, 1}.
-bool encode(CUtensorMap* m, double* base, const Geo& g, int box_rows, int box_pops) {
+CUtensorMapL2promotion promo_enum(int promo) {
+  return promo == 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+         : promo == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+         : promo == 64  ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                        : CU_TENSOR_MAP_L2_PROMOTION_NONE;
+}
+
+bool encode(CUtensorMap* m, double* base, const Geo& g, int box_rows, int box_pops, int promo) {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
     void* p = nullptr;
@@ -503,7 +578,7 @@ bool encode(CUtensorMap* m, double* base, const Geo& g, int box_rows, int box_po
   const cuuint32_t box[3] = {(cuuint32_t)box_rows, (cuuint32_t)box_pops, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_SWIZZLE_NONE, promo_enum(promo),
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -523,11 +598,15 @@ cudaError_t launch_tb(const Geo& g, const TbMaps* t, int src_buf, double* B, con
     if (dev < 64) done_mask |= 1ull << dev;
   }
   if (peers && !t->staged) return cudaErrorInvalidValue;
-  const CUtensorMap& stl = peers ? t->st[0] : t->load[src_buf];
-  const CUtensorMap& str = peers ? t->st[1] : t->load[src_buf];
-  kern<<<tb_grid(g, grid), Cfg::NT, Cfg::SMEM, s>>>(t->load[src_buf], t->pf[src_buf], B, g, r,
-                                                    (g.ly + TB_HT - 1) / TB_HT, l2_dist, thermal, wall_w16, mon,
-                                                    stl, str, peers);
+  TbKMaps km;
+  for (int c = 0; c < 3; ++c) {
+    km.src[c] = t->load[src_buf][c];
+    km.stL[c] = peers ? t->st[0][c] : t->load[src_buf][c];
+    km.stR[c] = peers ? t->st[1][c] : t->load[src_buf][c];
+  }
+  km.pf = t->pf[src_buf];
+  kern<<<tb_grid(g, grid), Cfg::NT, Cfg::SMEM, s>>>(km, B, g, r, (g.ly + TB_HT - 1) / TB_HT, l2_dist, thermal,
+                                                    wall_w16, mon, peers);
   return cudaGetLastError();
 }
 
@@ -540,16 +619,33 @@ int tb_grid(const Geo& g, int grid) {
   return (int)std::min<int64_t>(grid, U);
 }
 
-TbMaps* tb_create(const Geo& g, double* buf0, double* buf1) {
+bool encode_buffers(TbMaps* t, const Geo& g) {
+  for (int k = 0; k < 2; ++k)
+  {
+    for (int c = 0; c < 3; ++c)
+      if (!encode(&t->load[k][c], t->bufs[k], g, Cfg::RB, CLS_N[c], t->promo)) return false;
+    if (!encode(&t->pf[k], t->bufs[k], g, TB_HT + 16, Q, t->promo)) return false;
+  }
+  return true;
+}
+
+TbMaps* tb_create(const Geo& g, double* buf0, double* buf1, int promo) {
   if (g.y0 % 2 || g.nyp % 2 || g.lx < 2 * H) return nullptr;
   auto* t = new TbMaps();
-  double* bufs[2] = {buf0, buf1};
-  for (int k = 0; k < 2; ++k)
-    if (!encode(&t->load[k], bufs[k], g, Cfg::R0, 1) || !encode(&t->pf[k], bufs[k], g, TB_HT + 16, Q)) {
-      delete t;
-      return nullptr;
-    }
+  t->promo = promo;
+  t->bufs[0] = buf0;
+  t->bufs[1] = buf1;
+  if (!encode_buffers(t, g)) {
+    delete t;
+    return nullptr;
+  }
   return t;
+}
+
+bool tb_set_promotion(TbMaps* t, const Geo& g, int promo) {
+  t->promo = promo;
+  if (!encode_buffers(t, g)) return false;
+  return !t->staged || tb_attach_staging(t, g, t->stage);
 }
 
 void tb_destroy(TbMaps* t) { delete t; }
@@ -620,7 +716,11 @@ __global__ void __launch_bounds__(256) k_tb_pull(double2* __restrict__ stage, co
 bool tb_attach_staging(TbMaps* t, const Geo& g, double* stage) {
   Geo g6 = g;
   g6.nx = 6;  // 6 columns per side
-  if (!encode(&t->st[0], stage, g6, Cfg::R0, 1) || !encode(&t->st[1], stage + 6 * g.cs, g6, Cfg::R0, 1)) return false;
+  for (int c = 0; c < 3; ++c)
+    if (!encode(&t->st[0][c], stage, g6, Cfg::RB, CLS_N[c], t->promo) ||
+        !encode(&t->st[1][c], stage + 6 * g.cs, g6, Cfg::RB, CLS_N[c], t->promo))
+      return false;
+  t->stage = stage;
   t->staged = true;
   return true;
 }

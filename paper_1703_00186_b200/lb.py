@@ -86,9 +86,13 @@ def lib():
         return _lib
     import torch  # noqa: F401  (loads the wheel's libnccl.so.2 / CUDA runtime first)
     from . import _build
-    if _build.needs_build():
-        _build.build()
-    L = ctypes.CDLL(SO_PATH)
+    alt = os.environ.get("LB_D2Q37_LIB")  # tools only: a variant build of the same sources
+    if alt:
+        L = ctypes.CDLL(alt)
+    else:
+        if _build.needs_build():
+            _build.build()
+        L = ctypes.CDLL(SO_PATH)
     p, i, d, vp = ctypes.POINTER, ctypes.c_int, ctypes.c_double, ctypes.c_void_p
     sig = {
         "lb_query_layout": (i, [p(lb_params), i, i, p(lb_layout)]),
@@ -439,16 +443,20 @@ class Lattice:
         """Replay 2-step CUDA graphs in lb_step (needs a non-default stream)."""
         _check(lib().lb_set_option(self._ctx, 2, int(enable)))
 
-    def temporal(self, enable: bool = True, grid: int = 0, l2_prefetch: int = 0, wall_weight16: int = 20):
+    def temporal(self, enable: bool = True, grid: int = 0, l2_prefetch: int = 0, wall_weight16: int = 20,
+                 l2_promotion: int | None = None):
         """Two steps per pass over HBM (LB_OPT_TEMPORAL, the default where it
         applies: N = 1, walls, fused mode, monitors off):
         lb_step advances pairs of steps with the two-step kernel.  grid: CTAs
         (0 = one per SM); l2_prefetch: L2 prefetch distance in columns (0 = off);
-        wall_weight16: cost of a wall-strip column, x16, for the work split."""
+        wall_weight16: cost of a wall-strip column, x16, for the work split;
+        l2_promotion: L2 promotion of its TMA loads in bytes (None = library default)."""
         _check(lib().lb_set_option(self._ctx, 3, int(enable)))
         _check(lib().lb_set_option(self._ctx, 4, int(grid)))
         _check(lib().lb_set_option(self._ctx, 5, int(l2_prefetch)))
         _check(lib().lb_set_option(self._ctx, 6, int(wall_weight16)))
+        if l2_promotion is not None:
+            _check(lib().lb_set_option(self._ctx, 7, int(l2_promotion)))
 
     def monitor(self, enable: bool = True):
         """Fused monitors: invariants reduced inside the step kernel (lb_monitor)."""

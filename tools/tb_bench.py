@@ -17,11 +17,11 @@ import lbgen  # noqa: E402
 import paper_1703_00186_b200 as lbm  # noqa: E402
 
 
-def run(lx, ly, tb, grid=0, l2=0, k=200, coll="bgk", ww=20):
+def run(lx, ly, tb, grid=0, l2=0, k=200, coll="bgk", ww=20, promo=None):
     s = torch.cuda.Stream()
     g = lbm.Lattice(lx, ly, collision=coll, stream=s, temporal=False)
     if tb:
-        g.temporal(True, grid=grid, l2_prefetch=l2, wall_weight16=ww)
+        g.temporal(True, grid=grid, l2_prefetch=l2, wall_weight16=ww, l2_promotion=promo)
     g.init_macro(*lbgen.rt_macro(lx, ly, 1.0 / 1.19697977039307435897239 ** 2))
     g.step(20)
     g.sync()
@@ -55,6 +55,15 @@ def main():
         ms, ml, out = run(lx, ly, True, 0, 0, ww=ww)
         print(json.dumps({"tb": 1, "wall_w16": ww, "ms_per_step": ms, "mlups": ml,
                           "bit_identical": bool(np.array_equal(out, ref))}), flush=True)
+    promos = [int(x) for x in os.environ.get("TB_PROMO", "").split(",") if x]
+    if promos:
+        _, _, ref_c = run(lx, ly, False, coll="regularized")
+    for promo in promos:
+        for coll in ("bgk", "regularized"):
+            ms, ml, out = run(lx, ly, True, 0, 0, coll=coll, promo=promo)
+            print(json.dumps({"tb": 1, "l2_promotion": promo, "coll": coll, "ms_per_step": ms, "mlups": ml,
+                              "bit_identical": bool(np.array_equal(out, ref if coll == "bgk" else ref_c))}),
+                  flush=True)
     for coll in ("regularized",):
         ms, ml, ref = run(lx, ly, False, coll=coll)
         print(json.dumps({"tb": 0, "coll": coll, "mlups": ml}), flush=True)
