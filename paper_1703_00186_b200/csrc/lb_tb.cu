@@ -18,7 +18,10 @@
 //     [ya - 3 - cy, ya + HT + 3 - cy); ya even, so the box starts on 16 bytes,
 //     the TMA alignment rule of tools/tma_probe.cu), RB = HT + 12 rows.  The
 //     TMA coordinates perform the whole x-pull (propagate), so the state-n
-//     ring is just PF + 1 buffers.  7 loads per column, one per issuing lane;
+//     ring is just NB = PF + 1 = 2 buffers.  7 loads per column, one per
+//     issuing lane.  The phase-1 warps refill the buffer they just gathered
+//     from (named barrier 2 among them, then their lanes issue the loads of
+//     iteration t + NB), so a load has ~2 iterations in flight (EARLY);
 //   * phase 1 (warps [0, NW1)): state n+1 at column c1 = xs - 3 + t for the
 //     R1 = HT + 6 rows [ya - 3, ya + HT + 3) (the ±3-row apron step n+2 pulls
 //     from), written to the state-(n+1) ring;
@@ -331,6 +334,9 @@ __device__ __forceinline__ void phase2(const double* s1, double* __restrict__ B,
 #define LB_TB_HT 104
 #define LB_TB_PF 1
 #endif
+#ifndef LB_TB_EARLY
+#define LB_TB_EARLY 1
+#endif
 constexpr int TB_HT = LB_TB_HT;
 constexpr int TB_PF = LB_TB_PF;
 using Cfg = TbCfg<TB_HT, TB_PF>;
@@ -363,9 +369,11 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
                int l2_dist, int thermal, int wall_w16, double* __restrict__ mon, int peers) {
   using C = TbCfg<HT, PF>;
   constexpr int RB = C::RB, BUFD = C::BUFD, R1 = C::R1, NB = C::NB;
-  // PF = 0: one state-n buffer, refilled by the phase-1 warps right after they
-  // gathered from it (the TMA then overlaps their collisions)
-  constexpr bool EARLY = PF == 0;
+  // EARLY (LB_TB_EARLY, or PF = 0): the phase-1 warps refill the buffer they
+  // just gathered from with the windows of iteration t + NB (a named barrier
+  // among them, then their lanes issue), so a load has ~NB iterations in
+  // flight instead of PF
+  constexpr bool EARLY = PF == 0 || LB_TB_EARLY;
   extern __shared__ __align__(128) double sm[];
   double* s0 = sm;
   double* s1 = sm + C::S0_DBL;
@@ -466,7 +474,7 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
     const bool issuer = warp < NWI && (tid & 31) < GPW && my_grp < NG;
 
     if (issuer)
-      for (int k = 0; k < (EARLY ? 1 : PF) && k < nload; ++k) issue_one(k, my_grp);
+      for (int k = 0; k < (EARLY ? NB : PF) && k < nload; ++k) issue_one(k, my_grp);
 
     for (int t = 0; t < niter; ++t) {
       __syncthreads();  // every read of iteration t-1 is done: the buffers refilled below are free
@@ -502,11 +510,11 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
           const bool own = t >= 3 && t < W + 3 && y >= own_lo && y < own_hi;
           if (EARLY) {
             // gather, then (all phase-1 warps done reading) refill the buffer
-            // with iteration t + 1's windows while the collisions run
+            // with iteration t + NB's windows while the collisions run
             double f[Q];
             phase1_gather<BUFD, RB>(s0, buf, valid ? i : 0, f);
             asm volatile("bar.sync 2, %0;" ::"r"(32 * C::NW1) : "memory");
-            if (issuer && t + 1 < nload) issue_one(t + 1, my_grp);
+            if (issuer && t + NB < nload) issue_one(t + NB, my_grp);
             if (valid) phase1_update<COLL, R1, MON>(f, s1, t, i, y, ly, thermal, r, own, acc);
           } else if (valid) {
             phase1<COLL, BUFD, RB, R1, MON>(s0, s1, buf, t, i, y, ly, thermal, r, own, acc);

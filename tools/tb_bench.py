@@ -55,6 +55,11 @@ def main():
         ms, ml, out = run(lx, ly, True, 0, 0, ww=ww)
         print(json.dumps({"tb": 1, "wall_w16": ww, "ms_per_step": ms, "mlups": ml,
                           "bit_identical": bool(np.array_equal(out, ref))}), flush=True)
+    for combo in [x for x in os.environ.get("TB_COMBOS", "").split(",") if x]:
+        grid, ww = (int(v) for v in combo.split(":"))
+        ms, ml, out = run(lx, ly, True, grid, 0, ww=ww)
+        print(json.dumps({"tb": 1, "grid": grid, "wall_w16": ww, "ms_per_step": ms, "mlups": ml,
+                          "bit_identical": bool(np.array_equal(out, ref))}), flush=True)
     promos = [int(x) for x in os.environ.get("TB_PROMO", "").split(",") if x]
     if promos:
         _, _, ref_c = run(lx, ly, False, coll="regularized")
