@@ -654,6 +654,28 @@ def test_two_step_kernel_bit_identical(lb, coll, bc, shape):
     assert np.array_equal(outs[0], outs[1])
 
 
+def test_two_step_kernel_l2_promotion(lb):
+    """LB_OPT_TB_L2_PROMOTION only changes how the window loads fill L2: every
+    legal value gives the same bits (also switched mid-run, which re-encodes
+    the tensor maps); other values are rejected."""
+    lx, ly = 24, 230
+    st = oracle_state(lx, ly, seed=11)
+    ref = lb.Lattice(lx, ly)
+    ref.set_state(st)
+    ref.step(4)
+    for promo in (0, 64, 128, 256):
+        g = lb.Lattice(lx, ly)
+        g.temporal(True, l2_promotion=promo)
+        g.set_state(st)
+        g.step(2)
+        g.temporal(True, l2_promotion=256 if promo != 256 else 0)
+        g.step(2)
+        assert np.array_equal(g.gather(), ref.gather()), promo
+        with pytest.raises(lb.LBError):
+            g.temporal(True, l2_promotion=32)
+        g.close()
+
+
 @pytest.mark.parametrize("grid,l2", [(1, 0), (7, 4), (300, 8)])
 def test_two_step_kernel_grid_and_prefetch(lb, grid, l2):
     """Any CTA count (one CTA sweeping everything, uneven ranges, more CTAs than
