@@ -85,7 +85,6 @@ cudaError_t launch_step_fused_tma(const Geo& g, const TmaMaps* t, int src_buf, c
 // written (the next step's wrap).
 struct TbMaps {
   CUtensorMap load[2][3];  // column-group windows, box {HT + 12, 3 | 5 | 7, 1}, per buffer
-  CUtensorMap pf[2];       // L2 prefetch of a column window, box {HT + 16, 37, 1}
   CUtensorMap st[2][3];    // N > 1: staging of the left / right neighbour's 6 edge columns
   bool staged = false;  // st[] encoded (tb_attach_staging)
   int promo = 0;        // L2 promotion of every map: 0 / 64 / 128 / 256 bytes (LB_OPT_TB_L2_PROMOTION)
@@ -111,7 +110,7 @@ bool tb_layout_ok(int ly);
 void tb_destroy(TbMaps* t);
 // lb_tb.cu's own copies of the wall constants and the Gram inverse
 cudaError_t tb_upload_constants(const double* k_bottom, const double* k_top, const double* ginv, cudaStream_t s);
-// grid: CTAs (one per SM); l2_dist: L2 prefetch distance in columns (0 = off);
+// grid: CTAs (one per SM); l2_dist: L2 prefetch distance in columns (0 = off; LSU prefetch);
 // wall_w16: cost of a wall-strip column in 1/16 of an interior one (work split);
 // mon != nullptr: monitors, 2 x tb_grid(g, grid) x 5 doubles of per-CTA
 // partials (state n+1, then state n+2)

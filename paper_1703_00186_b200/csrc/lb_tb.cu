@@ -29,7 +29,12 @@
 //     HT rows of the strip, gathered from the state-(n+1) ring, stored to B
 //     (and, for the 3+3 border columns, into B's halo: the next step's wrap).
 // Both phases of an iteration are independent (phase 2 lags by one column more
-// than the ±3 reach), so ONE __syncthreads per iteration orders everything.
+// than the ±3 reach), so ONE __syncthreads per iteration orders everything
+// (BGK).  The regularised kernel (LB_TB_DECOUPLE) hands the state-(n+1) ring
+// between the phases with mbarriers instead: phase 2 of iteration t waits
+// until phase 1 wrote iteration t-1 and releases its slots right after its
+// gather; phase 1 of iteration t waits for that release of iteration t-1, so
+// either phase can run up to one iteration ahead of the other.
 //
 // State-(n+1) ring.  Population l of column c1 is pulled by phase 2 at column
 // c1 + cx_l, cx_l + 4 iterations later: cx_l + 5 slots of R1 rows (185 slots
@@ -136,7 +141,8 @@ struct TbCfg {
   static constexpr int NB = PF + 1;                 // state-n buffers per population = mbarriers
   static constexpr int S0_DBL = NB * BUFD;
   static constexpr int S1_DBL = SLOTS1_BEFORE(Q) * R1;
-  static constexpr size_t SMEM = (size_t)(S0_DBL + S1_DBL) * sizeof(double) + NB * sizeof(uint64_t);
+  // mbarriers: NB TMA buffers + (LB_TB_DECOUPLE) 2 full + 2 empty ring barriers
+  static constexpr size_t SMEM = (size_t)(S0_DBL + S1_DBL) * sizeof(double) + (NB + 4) * sizeof(uint64_t);
   static_assert(RB % 2 == 0 && RB <= 256, "TMA box rows");
   static_assert(SMEM <= 232448, "shared memory per CTA");
   static_assert(NW <= 8, "two warps per scheduler at most (64 KB register file per scheduler)");
@@ -297,15 +303,18 @@ __device__ __forceinline__ void phase1(const double* s0, double* s1, int b, int 
   phase1_update<COLL, R1, MON>(f, s1, t, i, y, ly, thermal, r, own, acc);
 }
 
-template <int COLL, int R1, bool MON>
-__device__ __forceinline__ void phase2(const double* s1, double* __restrict__ B, const Geo& g, int t, int i,
-                                       int y, int c2, bool thermal, const Relax& r, bool own, double (&acc)[5],
-                                       bool wrap) {
-  const int ly = g.ly;
-  double f[Q];
+template <int R1>
+__device__ __forceinline__ void phase2_gather(const double* s1, int t, int i, double (&f)[Q]) {
   const int io = opaque(i);
 #pragma unroll
   for (int l = 0; l < Q; ++l) f[l] = s1[((t - 4 - CX(l)) % L1(l)) * R1 + SLOTS1_BEFORE(l) * R1 + io + 3 - CY(l)];
+}
+
+template <int COLL, bool MON>
+__device__ __forceinline__ void phase2_update(double (&f)[Q], double* __restrict__ B, const Geo& g, int y, int c2,
+                                              bool thermal, const Relax& r, bool own, double (&acc)[5],
+                                              bool wrap) {
+  const int ly = g.ly;
   if (thermal && (y < 3 || y >= ly - 3)) thermal_wall(f, y < 3 ? 0 : 1);
   Macro mm;
   Macro* mp = (MON && own) ? &mm : nullptr;
@@ -330,12 +339,26 @@ __device__ __forceinline__ void phase2(const double* s1, double* __restrict__ B,
   }
 }
 
+template <int COLL, int R1, bool MON>
+__device__ __forceinline__ void phase2(const double* s1, double* __restrict__ B, const Geo& g, int t, int i,
+                                       int y, int c2, bool thermal, const Relax& r, bool own, double (&acc)[5],
+                                       bool wrap) {
+  double f[Q];
+  phase2_gather<R1>(s1, t, i, f);
+  phase2_update<COLL, MON>(f, B, g, y, c2, thermal, r, own, acc, wrap);
+}
+
 #ifndef LB_TB_HT
 #define LB_TB_HT 104
 #define LB_TB_PF 1
 #endif
 #ifndef LB_TB_EARLY
 #define LB_TB_EARLY 1
+#endif
+// bit 0: BGK, bit 1: regularised collide (default: regularised only — the
+// decoupled hand-over measured +7 % there, -1 % to +1 % with BGK)
+#ifndef LB_TB_DECOUPLE
+#define LB_TB_DECOUPLE 2
 #endif
 constexpr int TB_HT = LB_TB_HT;
 constexpr int TB_PF = LB_TB_PF;
@@ -353,9 +376,9 @@ __constant__ int4 c_tb_grp[NG] = {
 
 // Kernel tensor maps (all __grid_constant__): the state-n group windows of the
 // source buffer per box class (3 / 5 / 7 populations), the same for the N > 1
-// staging of the left / right neighbour's edge columns, and the L2 prefetch box.
+// staging of the left / right neighbour's edge columns.
 struct alignas(64) TbKMaps {
-  CUtensorMap src[3], stL[3], stR[3], pf;
+  CUtensorMap src[3], stL[3], stR[3];
 };
 
 // Warps [0, NW1): phase 1; [NW1, NW1 + NW2): phase 2.
@@ -366,7 +389,8 @@ struct alignas(64) TbKMaps {
 template <int COLL, int HT, int PF, bool MON>
 __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
     k_step2_tb(const __grid_constant__ TbKMaps km, double* __restrict__ B, Geo g, Relax r, int nstrips,
-               int l2_dist, int thermal, int wall_w16, double* __restrict__ mon, int peers) {
+               int l2_dist, int thermal, int wall_w16, double* __restrict__ mon, int peers,
+               const double* __restrict__ Asrc) {
   using C = TbCfg<HT, PF>;
   constexpr int RB = C::RB, BUFD = C::BUFD, R1 = C::R1, NB = C::NB;
   // EARLY (LB_TB_EARLY, or PF = 0): the phase-1 warps refill the buffer they
@@ -374,6 +398,14 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
   // among them, then their lanes issue), so a load has ~NB iterations in
   // flight instead of PF
   constexpr bool EARLY = PF == 0 || LB_TB_EARLY;
+  // DECOUPLE (LB_TB_DECOUPLE): no CTA barrier per iteration; the state-(n+1)
+  // ring is handed between the phases with mbarriers, alternating between two
+  // per direction (item I = the CTA's iteration count): full[I & 1] — the
+  // phase-1 warps wrote item I; empty[I & 1] — the phase-2 warps finished
+  // gathering in iteration I (the slots phase 1 overwrites at I + 1).  A phase
+  // can run up to one iteration ahead of the other.
+  constexpr bool DECOUPLE = (LB_TB_DECOUPLE >> (COLL == COLL_REGULARIZED ? 1 : 0)) & 1;
+  static_assert(!DECOUPLE || EARLY, "decoupled phases need the phase-1 warps to issue the loads");
   extern __shared__ __align__(128) double sm[];
   double* s0 = sm;
   double* s1 = sm + C::S0_DBL;
@@ -384,6 +416,10 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
 
   if (tid == 0) {
     for (int i = 0; i < NB; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bars + i)));
+    for (int i = 0; i < 2; ++i) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bars + NB + i)), "r"(32 * C::NW1));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bars + NB + 2 + i)), "r"(32 * C::NW2));
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -408,6 +444,8 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
   int64_t u = unit_at(wtot * blockIdx.x / gridDim.x);
   const int64_t u_end = unit_at(wtot * (blockIdx.x + 1) / gridDim.x);
   uint32_t kglob = 0;  // load iterations of this CTA over all its sweeps (barrier phase)
+  uint32_t iglob = 0;  // DECOUPLE: iterations of this CTA over all its sweeps (ring items)
+  const uint32_t bar_full = smem_u32(bars + NB), bar_empty = smem_u32(bars + NB + 2);
   double acc[5] = {0.0, 0.0, 0.0, 0.0, INFINITY};  // MON: this thread's state (n+1 or n+2)
 
   while (u < u_end) {
@@ -441,13 +479,6 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
       if (gq == 0) {
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
                      "r"((uint32_t)(Q * RB * sizeof(double))));
-        if (l2_dist > 0 && k + l2_dist < nload) {
-          // the newest column any population of iteration k + l2_dist touches
-          const int pcol = wrap_col(c1 + l2_dist + 3, lx);
-          asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(&km.pf),
-                       "r"(rbase - 8), "r"(0), "r"(pcol)
-                       : "memory");
-        }
       }
       const int4 gp = c_tb_grp[gq];  // (box class, first label, slab offset, cx)
       const int cls = gp.x;
@@ -477,9 +508,23 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
       for (int k = 0; k < (EARLY ? NB : PF) && k < nload; ++k) issue_one(k, my_grp);
 
     for (int t = 0; t < niter; ++t) {
-      __syncthreads();  // every read of iteration t-1 is done: the buffers refilled below are free
+      const uint32_t I = iglob + (uint32_t)t;
+      if (!DECOUPLE) __syncthreads();  // every read of iteration t-1 is done: the buffers refilled below are free
+      if (l2_dist > 0 && t + l2_dist < nload) {
+        // L2 prefetch (LSU, not the TMA queue) of the newest column the loads
+        // of iteration t + l2_dist touch: rows [ya - 6, ya + HT + 6) of all 37
+        // planes, 8 lines of 128 B each; N > 1: slab columns only
+        const int j = xs + t + l2_dist;  // c1(t + l2_dist) + 3
+        if (!peers || j < lx + H) {
+          const double* col = Asrc + (int64_t)(peers ? j : wrap_col(j, lx)) * g.cs + (rbase - 6);
+          for (int q = tid; q < Q * 8; q += C::NT)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(col + (int64_t)(q >> 3) * g.nyp + (q & 7) * 16));
+        }
+      }
       if (!EARLY && issuer && t + PF < nload) issue_one(t + PF, my_grp);
       if (warp < C::NW1) {
+        // DECOUPLE: the slots written below were last read by phase 2 in I - 1
+        if (DECOUPLE && t > 0) mbar_wait(bar_empty + 8 * ((I - 1) & 1), ((I - 1) >> 1) & 1);
         if (t < nload) {
           // phase 1: state n+1 at column c1 = xs - 3 + t, rows [ya-3, ya+HT+3)
           const uint32_t kb = kglob + (uint32_t)t;
@@ -520,6 +565,19 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
             phase1<COLL, BUFD, RB, R1, MON>(s0, s1, buf, t, i, y, ly, thermal, r, own, acc);
           }
         }
+        if (DECOUPLE)  // item I written (every phase-1 thread arrives: release of its ring stores)
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar_full + 8 * (I & 1)) : "memory");
+      } else if (DECOUPLE) {
+        // phase 2 (decoupled): wait for item I - 1, gather, release the slots
+        if (t > 0) mbar_wait(bar_full + 8 * ((I - 1) & 1), ((I - 1) >> 1) & 1);
+        const int i = tid - 32 * C::NW1;
+        const int y = ya + i;
+        const bool valid = t >= 7 && i < HT && y < ly;
+        double f[Q];
+        if (t >= 7) phase2_gather<R1>(s1, t, valid ? i : 0, f);
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar_empty + 8 * (I & 1)) : "memory");
+        if (valid)
+          phase2_update<COLL, MON>(f, B, g, y, xs - 7 + t, thermal, r, y >= own_lo && y < own_hi, acc, !peers);
       } else if (t >= 7) {
         // phase 2: state n+2 at column c2 = xs - 7 + t, rows [ya, ya+HT)
         const int i = tid - 32 * C::NW1;
@@ -529,7 +587,14 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
                                 !peers);
       }
     }
+    if (DECOUPLE) {
+      // wait for the last item's hand-over too, so every barrier phase is
+      // observed before the next sweep re-arms it
+      const uint32_t last = iglob + (uint32_t)niter - 1;
+      mbar_wait((warp < C::NW1 ? bar_empty : bar_full) + 8 * (last & 1), (last >> 1) & 1);
+    }
     kglob += (uint32_t)nload;
+    iglob += (uint32_t)niter;
     __syncthreads();  // the next sweep refills every ring
   }
   if (MON) {
@@ -562,8 +627,7 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
   }
 }
 
-// TMA maps of one buffer: group windows (box {HT + 12, 3 | 5 | 7, 1}) and the
-// whole-column L2 prefetch box {HT + 16, 37, 1}.
+// TMA maps of one buffer: group windows (box {HT + 12, 3 | 5 | 7, 1}).
 CUtensorMapL2promotion promo_enum(int promo) {
   return promo == 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
          : promo == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
@@ -612,9 +676,8 @@ cudaError_t launch_tb(const Geo& g, const TbMaps* t, int src_buf, double* B, con
     km.stL[c] = peers ? t->st[0][c] : t->load[src_buf][c];
     km.stR[c] = peers ? t->st[1][c] : t->load[src_buf][c];
   }
-  km.pf = t->pf[src_buf];
   kern<<<tb_grid(g, grid), Cfg::NT, Cfg::SMEM, s>>>(km, B, g, r, (g.ly + TB_HT - 1) / TB_HT, l2_dist, thermal,
-                                                    wall_w16, mon, peers);
+                                                    wall_w16, mon, peers, t->bufs[src_buf]);
   return cudaGetLastError();
 }
 
@@ -632,7 +695,6 @@ bool encode_buffers(TbMaps* t, const Geo& g) {
   {
     for (int c = 0; c < 3; ++c)
       if (!encode(&t->load[k][c], t->bufs[k], g, Cfg::RB, CLS_N[c], t->promo)) return false;
-    if (!encode(&t->pf[k], t->bufs[k], g, TB_HT + 16, Q, t->promo)) return false;
   }
   return true;
 }

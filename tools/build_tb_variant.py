@@ -1,6 +1,6 @@
 """Build a variant of the library with another two-step-kernel tiling (tools only).
 
-python tools/build_tb_variant.py HT PF [EARLY]  ->  paper_1703_00186_b200/variants/liblb_ht<HT>_pf<PF>[_e1].so
+python tools/build_tb_variant.py HT PF [EARLY [NAME=VALUE ...]]  ->  paper_1703_00186_b200/variants/liblb_ht<HT>_pf<PF>[_e1].so
 (lb_tb.cu compiled with -DLB_TB_HT=HT -DLB_TB_PF=PF, linked with the default
 build's other objects).  Load it with LB_D2Q37_LIB=<path>.  PF = 0: one
 state-n buffer refilled right after the phase-1 gather; EARLY = 1: the PF + 1
@@ -18,7 +18,9 @@ from paper_1703_00186_b200 import _build  # noqa: E402
 def main():
     ht, pf = int(sys.argv[1]), int(sys.argv[2])
     early = int(sys.argv[3]) if len(sys.argv) > 3 else 0
-    tag = f"ht{ht}_pf{pf}" + (f"_e{early}" if early else "")
+    extra = sys.argv[4:]  # further NAME=VALUE defines, e.g. LB_TB_DECOUPLE=1
+    tag = f"ht{ht}_pf{pf}" + (f"_e{early}" if early else "") + "".join(
+        "_" + d.split("=")[0].replace("LB_TB_", "").lower() + d.split("=")[1] for d in extra)
     _build.build()
     nd = _build.nccl_dir()
     out = os.path.join(_build.HERE, "variants")
@@ -27,7 +29,7 @@ def main():
     flags = [_build.ARCH, "-O3", "-lineinfo", "-std=c++17", "--fmad=false", "--expt-relaxed-constexpr",
              "-Xcompiler", "-fPIC,-ffp-contract=off,-fno-fast-math", "-Xptxas", "-v,-warn-spills",
              "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nd, "include"),
-             f"-DLB_TB_HT={ht}", f"-DLB_TB_PF={pf}", f"-DLB_TB_EARLY={early}"]
+             f"-DLB_TB_HT={ht}", f"-DLB_TB_PF={pf}", f"-DLB_TB_EARLY={early}", *("-D" + d for d in extra)]
     src = os.path.join(_build.HERE, "csrc", "lb_tb.cu")
     r = subprocess.run(["nvcc", *flags, "-c", src, "-o", obj], capture_output=True, text=True)
     sys.stdout.write("\n".join(l for l in (r.stdout + r.stderr).splitlines()

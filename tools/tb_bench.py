@@ -17,7 +17,8 @@ import lbgen  # noqa: E402
 import paper_1703_00186_b200 as lbm  # noqa: E402
 
 
-def run(lx, ly, tb, grid=0, l2=0, k=200, coll="bgk", ww=20, promo=None):
+def run(lx, ly, tb, grid=0, l2=0, k=None, coll="bgk", ww=20, promo=None):
+    k = k or int(os.environ.get("TB_K", "200"))
     s = torch.cuda.Stream()
     g = lbm.Lattice(lx, ly, collision=coll, stream=s, temporal=False)
     if tb:
