@@ -189,6 +189,24 @@ struct Shell {
   double A0, A1, A2;
 };
 
+#ifdef LB_CONST_BANK
+// (variant build, tools/build_tb_variant.py ... LB_CONST_BANK=1) the per-shell
+// constants as constant-bank operands instead of 64-bit immediates (2 UMOV each)
+struct ShellK {
+  double k0, k1, k2, ka, kb, w;
+};
+constexpr ShellK shell_k(int s) {
+  const double x2 = A2 * (double)SHELL_C2(s);
+  return ShellK{0.5 * (x2 - 2.0), 0.25 * (4.0 - x2), 0.125 * ((x2 * x2 - 8.0 * x2) + 8.0), 0.5 * (x2 - 4.0),
+                0.25 * (x2 - 6.0), SHELL_W(s)};
+}
+static __constant__ ShellK c_shk[NSHELL] = {shell_k(0), shell_k(1), shell_k(2), shell_k(3),
+                                            shell_k(4), shell_k(5), shell_k(6), shell_k(7)};
+#define LB_SHK(s, f, expr) c_shk[s].f
+#else
+#define LB_SHK(s, f, expr) (expr)
+#endif
+
 __device__ __forceinline__ void shell_coeffs(double u2, double t, Shell (&sh)[NSHELL]) {
   const double tt = dmul(t, t);
   const double b1 = dfma(-0.5, u2, 1.0);                  // 1 - u2/2
@@ -197,11 +215,11 @@ __device__ __forceinline__ void shell_coeffs(double u2, double t, Shell (&sh)[NS
 #pragma unroll
   for (int s = 0; s < NSHELL; ++s) {
     const double x2 = A2 * (double)SHELL_C2(s);
-    const double k0 = 0.5 * (x2 - 2.0);
-    const double k1 = 0.25 * (4.0 - x2);
-    const double k2 = 0.125 * ((x2 * x2 - 8.0 * x2) + 8.0);
-    const double ka = 0.5 * (x2 - 4.0);
-    const double kb = 0.25 * (x2 - 6.0);
+    const double k0 = LB_SHK(s, k0, 0.5 * (x2 - 2.0));
+    const double k1 = LB_SHK(s, k1, 0.25 * (4.0 - x2));
+    const double k2 = LB_SHK(s, k2, 0.125 * ((x2 * x2 - 8.0 * x2) + 8.0));
+    const double ka = LB_SHK(s, ka, 0.5 * (x2 - 4.0));
+    const double kb = LB_SHK(s, kb, 0.25 * (x2 - 6.0));
     sh[s].A0 = dfma(t, dfma(u2, k1, k0), dfma(tt, k2, b0));
     sh[s].A1 = dfma(t, ka, b1);
     sh[s].A2 = dfma(t, kb, b2);
@@ -229,7 +247,7 @@ __device__ __forceinline__ void collide_site(double (&f)[Q], const Relax& r, Mac
   const double orho = dmul(omega, m.rho);
   double g[NSHELL];
 #pragma unroll
-  for (int s = 0; s < NSHELL; ++s) g[s] = dmul(orho, SHELL_W(s));
+  for (int s = 0; s < NSHELL; ++s) g[s] = dmul(orho, LB_SHK(s, w, SHELL_W(s)));
   constexpr double C3 = 1.0 / 6.0, C4 = 1.0 / 24.0;
 #pragma unroll
   for (int l = 0; l < Q / 2; ++l) {
