@@ -318,12 +318,13 @@ int lb_sync(lb_ctx* ctx);
  * context stream; ignored while profiling. */
 /* LB_OPT_TEMPORAL (value 1, the default for N = 1 with walls in fused mode;
  * 0 disables): lb_step advances two steps per pass over HBM where it can
- * (N = 1 without NCCL or peers, walls, fused mode, monitors off):
+ * (N = 1 without NCCL or peers, or N > 1 in peer mode; walls, fused mode;
+ * monitors on or off):
  * one launch of the two-step kernel computes states n+1 and n+2, keeping n+1
  * in shared memory (temporal blocking).  Bit-identical to two
  * fused steps; an odd remainder takes one fused step.  LB_OPT_TB_GRID: CTAs of
  * that kernel (0 = one per SM), LB_OPT_TB_L2_PREFETCH: L2 prefetch distance in
- * columns (0 = off, <= 64).  LB_OPT_TB_WALL_WEIGHT: cost of a column of a
+ * columns (0 = off, the default, <= 64; per-line prefetch of the newest column).  LB_OPT_TB_WALL_WEIGHT: cost of a column of a
  * wall strip relative to an interior one, x16 (work split; default 20).
  * LB_OPT_TB_L2_PROMOTION: L2 promotion of that kernel's TMA window loads in
  * bytes (0 = none, 64 = default, 128, 256); results do not depend on it. */

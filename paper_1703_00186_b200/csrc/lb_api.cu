@@ -807,8 +807,9 @@ static int graph_two_steps(lb_ctx* c) {
   return LB_OK;
 }
 
-// Two steps in one pass (lb_tb.cu): N = 1 without NCCL or peers, walls, fused
-// mode, monitors off.  Bit-identical to two fused steps.
+// Two steps in one pass (lb_tb.cu): N = 1 without NCCL or peers, or N > 1 in
+// peer mode (staged edge columns); walls, fused mode, with or without
+// monitors.  Bit-identical to two fused steps.
 static bool tb_usable(const lb_ctx* c) {
   const bool alone = c->nranks == 1 && !c->comm && !c->peers_on;  // N = 1 periodic wrap
   const bool staged = c->peers_on && c->tb && c->tb->staged;       // N > 1 peer mode
