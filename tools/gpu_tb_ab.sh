@@ -1,6 +1,6 @@
 #!/bin/bash
 # A/B of two-step kernel variants on one box, long runs (sustained clocks / power), alternating.
-for rep in 1 2; do
+for rep in $(seq ${TB_REPS:-2}); do
   for v in ${TB_VARIANTS:-default}; do
     if [ "$v" = default ]; then unset LB_D2Q37_LIB; else export LB_D2Q37_LIB=$PWD/paper_1703_00186_b200/variants/liblb_$v.so; fi
     echo "== $v rep $rep"
