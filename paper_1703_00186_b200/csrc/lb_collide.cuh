@@ -40,9 +40,10 @@ LB_HD constexpr double ipow(int c, int p) {
 // M'_a = (1 - omega) M_a(f) + omega rho m_p(ux, T) m_q(uy, T): the raw moments
 // of f blended with the Maxwellian moments that f_eq reproduces exactly
 // (m_k(u, T) = E[(u + sqrt(T) Z)^k], lattice units).
-// mo != nullptr: also hand out rho, j = (M_10, M_01) and e = M_20 + M_02 of the
-// pre-collision f (monitors, lb_tb.cu; ux, uy, T are not filled).
-__device__ __forceinline__ void collide_site_reg(double (&f)[Q], const Relax& r, Macro* mo = nullptr) {
+// hook(moments): rho, j = (M_10, M_01) and e = M_20 + M_02 of the pre-collision
+// f (monitors, lb_tb.cu; ux, uy, T are not filled).
+template <class Hook = NoHook>
+__device__ __forceinline__ void collide_site_reg(double (&f)[Q], const Relax& r, const Hook& hook = Hook{}) {
   const double omega = r.omega, one_m_omega = r.one_m_omega;
   // 1. column sums T[cx+3][q] = sum_{l: cx_l = cx} cy_l^q f_l
   double T[7][5];
@@ -91,11 +92,13 @@ __device__ __forceinline__ void collide_site_reg(double (&f)[Q], const Relax& r,
   }
   // 3. macroscopic fields (Eq. 2): rho, u, T = (e/rho - |u|^2)/2
   const double rho = M[0];
-  if (mo) {
-    mo->rho = rho;
-    mo->jx = M[6];
-    mo->jy = M[9];
-    mo->e = dadd(M[1], M[2]);
+  {
+    Macro mo;  // ux, uy, T not filled (the hook uses rho, j, e)
+    mo.rho = rho;
+    mo.jx = M[6];
+    mo.jy = M[9];
+    mo.e = dadd(M[1], M[2]);
+    hook(mo);
   }
   const double inv = __drcp_rn(rho);
   const double ux0 = dmul(M[6], inv), uy0 = dmul(M[9], inv);

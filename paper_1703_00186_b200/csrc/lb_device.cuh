@@ -232,12 +232,18 @@ __device__ __forceinline__ double cu_of(int l, double Ux, double Uy) {
   return dfma((double)CX(l), Ux, dmul((double)CY(l), Uy));
 }
 
-// f <- f - omega (f - f_eq(moments of f)), in registers.  mo != nullptr:
-// also hand out the moments of the pre-collision f (monitors, lb_tb.cu).
-__device__ __forceinline__ void collide_site(double (&f)[Q], const Relax& r, Macro* mo = nullptr) {
+// A collision hook sees the moments of the pre-collision f as soon as they are
+// formed (monitors, lb_tb.cu); the default does nothing.
+struct NoHook {
+  __device__ __forceinline__ void operator()(const Macro&) const {}
+};
+
+// f <- f - omega (f - f_eq(moments of f)), in registers; hook(moments).
+template <class Hook = NoHook>
+__device__ __forceinline__ void collide_site(double (&f)[Q], const Relax& r, const Hook& hook = Hook{}) {
   const double omega = r.omega, one_m_omega = r.one_m_omega;
   const Macro m = moments(f);
-  if (mo) *mo = m;
+  hook(m);
   const double ux = dadd(m.ux, r.tgx), uy = dadd(m.uy, r.tgy), Te = dadd(m.T, r.dT);
   const double Ux = dmul(A2, ux), Uy = dmul(A2, uy);
   const double u2 = dmul(A2, dfma(ux, ux, dmul(uy, uy)));

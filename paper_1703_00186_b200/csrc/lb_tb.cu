@@ -245,6 +245,15 @@ constexpr bool vrows_ok() {
 // two-step kernel is FP64-latency-bound).  They equal the sums over the stored
 // state up to rounding (tests: <= 1e-13 of the mass).
 __device__ __forceinline__ void acc_invariants(const Macro& m, const Relax& r, double (&a)[5]) {
+  if (r.tgx == 0.0 && r.tgy == 0.0 && r.dT == 0.0) {
+    // no body force (uniform branch): the increments below are exact zeros
+    a[0] = __dadd_rn(a[0], m.rho);
+    a[1] = __dadd_rn(a[1], m.jx);
+    a[2] = __dadd_rn(a[2], m.jy);
+    a[3] = __dadd_rn(a[3], __dmul_rn(0.5, m.e));
+    a[4] = fmin(a[4], m.rho != m.rho ? -INFINITY : m.rho);
+    return;
+  }
   const double djx = __dmul_rn(r.omega, __dmul_rn(m.rho, r.tgx));
   const double djy = __dmul_rn(r.omega, __dmul_rn(m.rho, r.tgy));
   const double tg2 = __fma_rn(r.tgx, r.tgx, __dmul_rn(r.tgy, r.tgy));
@@ -275,13 +284,14 @@ __device__ __forceinline__ void phase1_update(double (&f)[Q], double* s1, int t,
   const int io = opaque(i);
   const bool wall = y < 3 || y >= ly - 3;
   if (thermal && wall) thermal_wall(f, y < 3 ? 0 : 1);
-  Macro mm;
-  Macro* mp = (MON && own) ? &mm : nullptr;
-  if (COLL == COLL_REGULARIZED) collide_site_reg(f, r, mp);
-  else collide_site(f, r, mp);
+  // monitors: accumulated as soon as the collision has formed the moments
+  auto hook = [&](const Macro& m) {
+    if (MON && own) acc_invariants(m, r, acc);
+  };
+  if (COLL == COLL_REGULARIZED) collide_site_reg(f, r, hook);
+  else collide_site(f, r, hook);
 #pragma unroll
   for (int l = 0; l < Q; ++l) s1[(SLOTS1_BEFORE(l) + (t % L1(l))) * R1 + io] = f[l];
-  if (MON && own) acc_invariants(mm, r, acc);
   if (wall) {
     // virtual row of refl(l): -1 - y (bottom) or 2 ly - 1 - y (top); ring row
     // index = absolute row - (ya - 3), and i = y - (ya - 3)
@@ -316,11 +326,11 @@ __device__ __forceinline__ void phase2_update(double (&f)[Q], double* __restrict
                                               bool wrap) {
   const int ly = g.ly;
   if (thermal && (y < 3 || y >= ly - 3)) thermal_wall(f, y < 3 ? 0 : 1);
-  Macro mm;
-  Macro* mp = (MON && own) ? &mm : nullptr;
-  if (COLL == COLL_REGULARIZED) collide_site_reg(f, r, mp);
-  else collide_site(f, r, mp);
-  if (MON && own) acc_invariants(mm, r, acc);
+  auto hook = [&](const Macro& m) {
+    if (MON && own) acc_invariants(m, r, acc);
+  };
+  if (COLL == COLL_REGULARIZED) collide_site_reg(f, r, hook);
+  else collide_site(f, r, hook);
   // 64-bit stride: one IMAD.WIDE per store instead of IMAD + LEA + LEA.HI.X
   const int64_t nyp = opaque(g.nyp);
   double* p = B + (int64_t)c2 * g.cs + g.y0 + y;
