@@ -676,16 +676,18 @@ def test_two_step_kernel_l2_promotion(lb):
         g.close()
 
 
+@pytest.mark.parametrize("coll", ["bgk", "regularized"])
 @pytest.mark.parametrize("grid,l2", [(1, 0), (7, 4), (300, 8)])
-def test_two_step_kernel_grid_and_prefetch(lb, grid, l2):
+def test_two_step_kernel_grid_and_prefetch(lb, grid, l2, coll):
     """Any CTA count (one CTA sweeping everything, uneven ranges, more CTAs than
-    SMs) and any L2 prefetch distance give the same bits."""
+    SMs) and any L2 prefetch distance give the same bits — for the regularised
+    kernel this also runs its mbarrier hand-over across many sweeps per CTA."""
     lx, ly = 40, 150
     st = oracle_state(lx, ly, seed=5)
-    ref = lb.Lattice(lx, ly)
+    ref = lb.Lattice(lx, ly, collision=coll)
     ref.set_state(st)
     ref.step(6)
-    g = lb.Lattice(lx, ly)
+    g = lb.Lattice(lx, ly, collision=coll)
     g.temporal(True, grid=grid, l2_prefetch=l2)
     g.set_state(st)
     g.step(6)
