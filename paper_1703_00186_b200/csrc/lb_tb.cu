@@ -56,6 +56,10 @@
 #include "lb_device.cuh"
 #include "lb_internal.h"
 
+#ifndef LB_TB_STCS
+#define LB_TB_STCS 0
+#endif
+
 namespace lbk {
 using namespace lbd;
 
@@ -335,7 +339,13 @@ __device__ __forceinline__ void phase2_update(double (&f)[Q], double* __restrict
   const int64_t nyp = opaque(g.nyp);
   double* p = B + (int64_t)c2 * g.cs + g.y0 + y;
 #pragma unroll
-  for (int l = 0; l < Q; ++l) p[l * nyp] = f[l];
+  for (int l = 0; l < Q; ++l) {
+#if LB_TB_STCS  // variant: streaming (evict-first) stores of state n+2
+    __stcs(p + l * nyp, f[l]);
+#else
+    p[l * nyp] = f[l];
+#endif
+  }
   // N = 1 wrap of the next step: border columns also go to the halo
   if (wrap && c2 < 2 * H) {
     double* q = p + (int64_t)g.lx * g.cs;
