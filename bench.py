@@ -136,6 +136,32 @@ def oracle_throughput(lx_total: int, ly: int, budget_s: float):
     return mlups, oracle.threads(), sample, dt, w, nsteps
 
 
+def oracle_protocol():
+    """SURVEY §8d oracle timing protocol: the oracle as it stands on 64x32 x 10
+    steps and 1920x2048 x 3 steps (whole lattices, RT init), once with one
+    thread and once with OpenMP over ix on all the host cores it may use.
+    Returns {workload: {"threads_1": MLUPS, "threads_<n>": MLUPS, ...}}."""
+    import lbgen
+    import oracle
+    T0 = oracle.t0()
+    ncores = len(os.sched_getaffinity(0))
+    res = {"cores_available": ncores}
+    for lx, ly, nsteps in ((64, 32, 10), (1920, 2048, 3)):
+        key = f"{lx}x{ly}_{nsteps}steps"
+        res[key] = {}
+        for nt in (1, ncores):
+            oracle.set_threads(nt)
+            o = oracle.Lattice(lx, ly)
+            o.init_macro(*lbgen.rt_macro(lx, ly, T0))
+            t = time.perf_counter()
+            o.step(nsteps)
+            dt = time.perf_counter() - t
+            res[key][f"threads_{oracle.threads()}"] = round(lx * ly * nsteps / dt / 1e6, 3)
+            del o
+    oracle.set_threads(ncores)
+    return res
+
+
 def run_reference(args, cfg_name, lx_total, ly, scaling, rank, world):
     if rank != 0:
         return
@@ -335,6 +361,21 @@ def main():
     barrier()
     launches = g.launch_count() - launches0
     ms = max_over_ranks(e0.elapsed_time(e1))
+    # ---- spread (median over >= 5 repetitions): 5 more timed
+    # regions of max(K, 200) steps each, same protocol; the headline value
+    # stays the contract's region above
+    k_rep = max(args.steps, 200) // 2 * 2
+    reps = []
+    for _ in range(5):
+        barrier()
+        torch.cuda.synchronize()
+        r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        r0.record(stream)
+        g.step(k_rep)
+        r1.record(stream)
+        g.sync()
+        torch.cuda.synchronize()
+        reps.append(pm.mlups(lx_total * ly * k_rep, max_over_ranks(r0.elapsed_time(r1)) * 1e-3))
     g.profile(True)
     g.profile_reset()
     barrier()
@@ -403,6 +444,8 @@ def main():
         "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": workload_config(args.config, lx_total, ly, world, args.mode),
         "clocks": clk.summary(), "gpu_launches": int(launches),
+        "repetitions": {"regions": len(reps), "steps_each": k_rep, "median": round(statistics.median(reps), 2),
+                        "min": round(min(reps), 2), "max": round(max(reps), 2), "unit": "MLUPS"},
         "roofline": roofline,
         "kernel_times_ms": {k: {"avg_ms": v["total_ms"] / max(1, v["launches"]), "launches": v["launches"]}
                             for k, v in prof.items()},
@@ -421,7 +464,11 @@ def main():
         st0 = g.peek(0)
         host_in.numpy()[:] = st0.reshape(-1)
         del st0
-        k_e2e = max(10, min(args.steps, 1000)) // 2 * 2   # the same K as the timed region
+        # a user's run: upload once, K steps with one result per step read
+        # back, gather once.  K = max(timed K, 1000): at the driver's K = 20 the
+        # two 1.17 GB PCIe copies alone would be ~90 % of the region
+        # (e2e_at_timed_K below repeats it at the timed K for transparency)
+        k_e2e = max(args.steps, 1000) // 2 * 2
         g.monitor(True)   # per-step invariants reduced inside the step kernel (lb_monitor)
         mon = torch.empty((k_e2e, 5), dtype=torch.float64).pin_memory()   # per-step results on the host
         # the two-step kernel (default at N = 1 with walls) carries monitors of
@@ -466,6 +513,28 @@ def main():
                                  "lb_invariants_async -> pinned host) + lb_gather(pinned host)"),
                        "per_step_results_ok": bool(np.isfinite(m).all() and (m[:, 4] > 0).all()),
                        "mass_drift_over_K": mass_drift}
+        if k_e2e != args.steps // 2 * 2 and args.steps >= 2:
+            k2 = args.steps // 2 * 2
+            barrier()
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            g.set_state(host_in.numpy())
+            barrier()
+            for k in range(0, k2, 2 if pair else 1):
+                if pair:
+                    g.step(2)
+                    g.invariants_pair_async(mon[k:k + 2])
+                else:
+                    g.step(1)
+                    g.invariants_async(mon[k])
+            if same_gpu:
+                g.peek(0)
+            else:
+                g.gather(out=host_out.numpy() if host_out is not None else None)
+            dt2 = max_over_ranks(time.perf_counter() - t)
+            line["e2e_at_timed_K"] = {"value": round(sites_all * k2 / dt2 / 1e6, 2), "unit": "MLUPS", "steps": k2,
+                                      "h2d_bytes_per_step": state_bytes / k2,
+                                      "d2h_bytes_per_step": (state_bytes + 5 * 8 * k2) / k2}
         del host_in, host_out
         # ---- per-kernel passes (N = 1): split BGK (propagate GB/s, collide FP64 %),
         #      fused and split regularised collide (NEXT 1)
@@ -480,6 +549,8 @@ def main():
                                                                 float(os.environ.get("LB_CPU_BUDGET_S", "15")))
             line["cpu_baseline"] = {"value": round(mlups, 3), "unit": "MLUPS", "cores": cores,
                                     "kind": "oracle", "sample": sample}
+            if os.environ.get("LB_CPU_PROTOCOL", "1") == "1":
+                line["cpu_baseline"]["protocol"] = oracle_protocol()
 
     if rank == 0:
         print(json.dumps(line), flush=True)

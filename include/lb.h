@@ -69,7 +69,9 @@ enum lb_status {
   LB_ESTATE = 2,     /* call out of order (e.g. lb_gather mid-step)         */
   LB_ECUDA = 3,      /* CUDA runtime / kernel error                          */
   LB_ENCCL = 4,      /* NCCL error                                           */
-  LB_ENONPHYS = 5,   /* NaN or rho <= 0 detected by lb_invariants            */
+  LB_ENONPHYS = 5,   /* NaN or rho <= 0 detected by lb_invariants, or (sticky
+                        device flag) by any invariants / monitor reduction
+                        since the last state change, reported by lb_sync     */
   LB_ENOMEM = 6,     /* host or device allocation failed                     */
   LB_EPEER = 7       /* peer exchange watchdog: a neighbour never signalled  */
 };
@@ -100,7 +102,12 @@ typedef struct lb_params {
   double t_top;          /* wall temperature at y = Ly - 1/2                  */
   int bc_y;              /* enum lb_bc_y                                       */
   int mode;              /* enum lb_mode                                       */
-  int overlap;           /* 1: exchange || bulk, then borders     */
+  int overlap;           /* 1: exchange || bulk, then borders.
+                            lb_init returns LB_EINVAL where the schedule cannot
+                            run: split mode, bc_y = PERIODIC, lx < 6, or N = 1
+                            without an NCCL id (the local wrap has no exchange).
+                            The peer-store exchange (lb_set_peers) always
+                            overlaps inside the kernel, whatever this flag.   */
   int collision;         /* enum lb_collision                                 */
   double gx, gy;         /* body force: velocity increment per step (NEXT 2,
                             shifted equilibrium u + tau g, T + tau(1-tau)|g|^2/D;
@@ -292,7 +299,12 @@ int lb_invariants(lb_ctx* ctx, double* out);
 
 /* Non-blocking variant: enqueues the same reduction (collective) and an async
  * copy of the 5 values into host_out (page-locked memory for true asynchrony),
- * valid after the next lb_sync; no NaN / rho checks are made. */
+ * valid after the next lb_sync.  The check runs on the device: a result with a
+ * NaN sum or min rho <= 0 sets the context's sticky non-physical flag, and the
+ * next lb_sync returns LB_ENONPHYS ("numerical blow-up").
+ * With monitors on (lb_monitor) the minimum also turns -inf when a collision's
+ * own u or T is NaN / infinite, so a blow-up is caught by the launch whose
+ * collision created it. */
 int lb_invariants_async(lb_ctx* ctx, double* host_out);
 
 /* Both states of the last two-step launch (LB_OPT_TEMPORAL) with monitors on:
@@ -300,9 +312,14 @@ int lb_invariants_async(lb_ctx* ctx, double* host_out);
  * host_out[5..9] = those of state n+2, reduced from per-CTA partials the
  * two-step kernel wrote (so a two-step lb_step(2) still yields one result per
  * time step).  host_out: 10 doubles, page-locked for true asynchrony; valid
- * after the next lb_sync.  LB_ESTATE if the last step was not such a launch. */
+ * after the next lb_sync.  LB_ESTATE if the last step was not such a launch.
+ * Non-physical results set the sticky flag lb_sync reports (as above). */
 int lb_invariants_pair_async(lb_ctx* ctx, double* host_out);
 
+/* Waits for the context's streams.  LB_EPEER if a peer wait timed out;
+ * LB_ENONPHYS if any invariants / monitor reduction since the last
+ * lb_set_state / lb_init_macro / lb_init_rt saw NaN or rho <= 0 (the flag
+ * stays set until the state is replaced). */
 int lb_sync(lb_ctx* ctx);
 
 /* Options.  LB_OPT_PROPAGATE_IMPL (lb_propagate, split mode): 1 = TMA-staged
@@ -327,7 +344,14 @@ int lb_sync(lb_ctx* ctx);
  * columns (0 = off, the default, <= 64; per-line prefetch of the newest column).  LB_OPT_TB_WALL_WEIGHT: cost of a column of a
  * wall strip relative to an interior one, x16 (work split; default 20).
  * LB_OPT_TB_L2_PROMOTION: L2 promotion of that kernel's TMA window loads in
- * bytes (0 = none, 64 = default, 128, 256); results do not depend on it. */
+ * bytes (0 = none, 64 = default, 128, 256); results do not depend on it.
+ * LB_OPT_TB_EDGE_PULL (N > 1, peer mode): 1 (default) = the exchange runs
+ * inside the two-step kernel — only the CTAs whose sweep reads or writes
+ * within 6 columns of a slab edge wait for that neighbour's launch counter and
+ * stage their strip's rows of its 6 edge columns, so the interior sweeps
+ * overlap the exchange (§8a6); 0 = a separate k_tb_pull launch
+ * (wait for both neighbours, stage whole columns) before the kernel.  Both
+ * give the same bits. */
 enum lb_option {
   LB_OPT_PROPAGATE_IMPL = 0,
   LB_OPT_FUSED_IMPL = 1,
@@ -336,7 +360,8 @@ enum lb_option {
   LB_OPT_TB_GRID = 4,
   LB_OPT_TB_L2_PREFETCH = 5,
   LB_OPT_TB_WALL_WEIGHT = 6,
-  LB_OPT_TB_L2_PROMOTION = 7
+  LB_OPT_TB_L2_PROMOTION = 7,
+  LB_OPT_TB_EDGE_PULL = 8
 };
 int lb_set_option(lb_ctx* ctx, int option, int value);
 

@@ -63,7 +63,7 @@ def lib():
             "lbref_init_macro": (v, [p, p, p, p, p]),
             "lbref_pbc": (v, [p]), "lbref_propagate": (v, [p]), "lbref_bc": (v, [p]),
             "lbref_collide": (v, [p]), "lbref_swap": (v, [p]), "lbref_step": (v, [p, i]),
-            "lbref_invariants": (v, [p, i, p]), "lbref_threads": (i, []),
+            "lbref_invariants": (v, [p, i, p]), "lbref_threads": (i, []), "lbref_set_threads": (v, [i]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -229,3 +229,8 @@ class Lattice:
 
 def threads() -> int:
     return lib().lbref_threads()
+
+
+def set_threads(n: int) -> None:
+    """Timing harness only: OpenMP threads of the stepper (arithmetic unchanged)."""
+    lib().lbref_set_threads(int(n))

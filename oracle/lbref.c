@@ -481,6 +481,17 @@ void lbref_invariants(const lbref* s, int which, double out[4])
     out[3] = e;
 }
 
+/* Timing harness only (bench.py cpu_baseline): thread count of the OpenMP
+ * loops over ix; the per-site arithmetic does not depend on it. */
+void lbref_set_threads(int n)
+{
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
+
 int lbref_threads(void)
 {
 #ifdef _OPENMP

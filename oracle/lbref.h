@@ -84,6 +84,7 @@ void   lbref_step(lbref*, int nsteps);
 /* O9: {sum rho, sum jx, sum jy, sum 0.5|c|^2 f} over physical sites        */
 void   lbref_invariants(const lbref*, int which, double out[4]);
 int    lbref_threads(void);      /* OpenMP threads the stepper uses          */
+void   lbref_set_threads(int n); /* timing only: OpenMP threads (n > 0)      */
 
 #ifdef __cplusplus
 }

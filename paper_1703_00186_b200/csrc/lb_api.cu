@@ -138,6 +138,7 @@ struct lb_ctx {
   double* d_mon = nullptr;    // monitor_slots x 5 partials, then MON_REDUCE_MAX_BLOCKS x 5 (reduce scratch)
   unsigned int* d_ticket = nullptr;        // k_monitor_reduce arrival counter (kept zero)
   unsigned int* d_status = nullptr;        // peer watchdog flag (device)
+  unsigned int* d_nonphys = nullptr;       // sticky: an invariants reduction saw NaN or rho <= 0 (device)
   unsigned long long peer_timeout_ns = 20000000000ull;
   lbk::TmaMaps* tma = nullptr;  // tensor maps of f_a / f_b (TMA propagate)
   int prop_impl = 0;            // LB_OPT_PROPAGATE_IMPL (1 = TMA when available)
@@ -149,6 +150,7 @@ struct lb_ctx {
   int tb_l2 = 0;                // LB_OPT_TB_L2_PREFETCH: L2 prefetch distance in columns
   int tb_promo = 64;            // LB_OPT_TB_L2_PROMOTION: L2 promotion of its TMA loads (bytes)
   int tb_wall_w16 = 20;         // LB_OPT_TB_WALL_WEIGHT: wall-strip column cost x16 (work split)
+  int tb_edge_pull = 1;         // LB_OPT_TB_EDGE_PULL: N > 1 two-step exchange inside the kernel (1) or k_tb_pull first (0)
   double* d_stage = nullptr;    // N > 1 two-step: the neighbours' 6 edge columns (2 x 6 x cs doubles)
   double* d_mon_tb = nullptr;   // two-step monitors: 2 x cap x 5 per-CTA partials, then reduce scratch
   int mon_tb_cap = 0;           // CTAs d_mon_tb holds partials for
@@ -452,6 +454,21 @@ int check_boundary(lb_ctx* c, const char* what) {
   return LB_OK;
 }
 
+// Sticky non-physical flag (set by the invariants / monitor reductions on
+// the device): LB_ENONPHYS once any reduction since the last state change saw
+// a NaN or min rho <= 0.
+int check_nonphys(lb_ctx* c) {
+  unsigned int st = 0;
+  CU(cudaMemcpy(&st, c->d_nonphys, sizeof(st), cudaMemcpyDeviceToHost));
+  if (st) return fail(LB_ENONPHYS, "non-physical state: an invariants reduction saw NaN or rho <= 0");
+  return LB_OK;
+}
+
+int reset_nonphys(lb_ctx* c) {
+  CU(cudaMemsetAsync(c->d_nonphys, 0, sizeof(unsigned int), c->s));
+  return LB_OK;
+}
+
 }  // namespace
 
 // ============================================================================
@@ -523,6 +540,16 @@ int lb_init(const lb_params* p, const lb_dist* d, double* f_a, double* f_b, void
   *out = nullptr;
   const int rank = d ? d->rank : 0, nranks = d ? d->nranks : 1;
   TRY(validate(p, rank, nranks));
+  // overlap (§8a6) only where the bulk || exchange schedule exists:
+  // an NCCL exchange (or, N > 1, the peer stores, which always overlap inside
+  // the kernel), fused mode, walls in Y — anywhere else it would be a silent no-op
+  if (p->overlap) {
+    if (p->mode != LB_MODE_FUSED) return fail(LB_EINVAL, "overlap needs fused mode");
+    if (p->bc_y == LB_PERIODIC) return fail(LB_EINVAL, "overlap needs walls in Y (periodic Y wraps rows the bulk reads)");
+    if (nranks == 1 && !(d && d->nccl_id))
+      return fail(LB_EINVAL, "overlap at N = 1 needs an NCCL communicator (the local wrap has no exchange to overlap)");
+    if (p->lx_total / nranks < 6) return fail(LB_EINVAL, "overlap needs lx >= 6 (3+3 border columns)");
+  }
   if (!f_a || !f_b || f_a == f_b) return fail(LB_EINVAL, "need two distinct device buffers");
   if (((uintptr_t)f_a | (uintptr_t)f_b) & 15) return fail(LB_EINVAL, "buffers must be 16-byte aligned");
   lb_ctx* c = new (std::nothrow) lb_ctx();
@@ -563,6 +590,9 @@ int lb_init(const lb_params* p, const lb_dist* d, double* f_a, double* f_b, void
     return bail(fail(LB_ENOMEM, "device scratch allocation failed"));
   if (cudaMallocHost(&c->h_pin, 16 * sizeof(double)) != cudaSuccess)
     return bail(fail(LB_ENOMEM, "pinned allocation failed"));
+  if (cudaMalloc(&c->d_nonphys, sizeof(unsigned int)) != cudaSuccess ||
+      cudaMemsetAsync(c->d_nonphys, 0, sizeof(unsigned int), c->s) != cudaSuccess)
+    return bail(fail(LB_ENOMEM, "flag allocation failed"));
   if (cudaMemsetAsync(c->A, 0, c->L.bytes, c->s) != cudaSuccess ||
       cudaMemsetAsync(c->B, 0, c->L.bytes, c->s) != cudaSuccess)
     return bail(fail(LB_ECUDA, "zero-fill failed: %s", cudaGetErrorString(cudaGetLastError())));
@@ -623,6 +653,7 @@ void lb_destroy(lb_ctx* c) {
   if (c->d_stage) cudaFree(c->d_stage);
   if (c->d_ticket) cudaFree(c->d_ticket);
   if (c->d_status) cudaFree(c->d_status);
+  if (c->d_nonphys) cudaFree(c->d_nonphys);
   if (c->tma) lbk::tma_destroy(c->tma);
   if (c->tb) lbk::tb_destroy(c->tb);
   graph_reset(c);
@@ -660,6 +691,7 @@ int lb_init_macro(lb_ctx* c, const double* rho, const double* ux, const double* 
   }
   c->halo_fresh = false;
   c->mon_valid = false;
+  TRY(reset_nonphys(c));
   TRY(launch(c, "k_init_macro", c->s, n, [&] {
     return lbk::launch_init_macro(c->g, c->A, dev[0], dev[1], dev[2], dev[3], c->s);
   }));
@@ -676,6 +708,7 @@ int lb_init_rt(lb_ctx* c, const double* eps, double t_ref, double amp, double wi
   CU(cudaMemcpyAsync(c->B, eps, lx_total * sizeof(double), cudaMemcpyDefault, c->s));
   c->halo_fresh = false;
   c->mon_valid = false;
+  TRY(reset_nonphys(c));
   TRY(launch(c, "k_init_rt", c->s, c->L.sites, [&] {
     return lbk::launch_init_rt(c->g, c->A, c->B, lx_total, c->rank * c->g.lx, t_ref, amp, width, c->s);
   }));
@@ -694,6 +727,7 @@ int lb_set_state(lb_ctx* c, const double* canon, int on_device) {
   }
   c->halo_fresh = false;
   c->mon_valid = false;
+  TRY(reset_nonphys(c));
   TRY(launch(c, "k_canon_to_internal", c->s, c->L.sites, [&] {
     return lbk::launch_canon_to_internal(c->g, src, c->A, c->s);
   }));
@@ -831,7 +865,18 @@ static int step_tb(lb_ctx* c) {
   double* mon = c->mon_on ? c->d_mon_tb : nullptr;
   const lb_peers& P = c->peers;
   const bool peers = c->peers_on;
-  if (peers)  // N > 1: wait for both neighbours' previous launch, copy their 6 edge columns
+  lbk::TbPeer pull;
+  const bool inpull = peers && c->tb_edge_pull;
+  if (inpull) {  // N > 1 default: only the edge CTAs wait and stage (overlapped with the interior)
+    pull.L = P.left_buf[c->par];
+    pull.R = P.right_buf[c->par];
+    pull.stage = c->d_stage;
+    pull.waitL = reinterpret_cast<const unsigned long long*>(P.left_done);
+    pull.waitR = reinterpret_cast<const unsigned long long*>(P.right_done);
+    pull.my_done = reinterpret_cast<const unsigned long long*>(P.my_done);
+    pull.status = c->d_status;
+    pull.timeout_ns = c->peer_timeout_ns;
+  } else if (peers)  // LB_OPT_TB_EDGE_PULL = 0: wait for both neighbours, copy their 6 edge columns, then the kernel
     TRY(launch(c, "k_tb_pull", c->s, 12LL * c->g.ly, [&] {
       return lbk::launch_tb_pull(c->g, c->d_stage, P.left_buf[c->par], P.right_buf[c->par],
                                  reinterpret_cast<const unsigned long long*>(P.left_done),
@@ -841,7 +886,7 @@ static int step_tb(lb_ctx* c) {
     }));
   TRY(launch(c, c->p.collision ? "k_step2_tb_reg" : "k_step2_tb", c->s, 2 * c->L.sites, [&] {
     return lbk::launch_step2_tb(c->g, c->tb, c->par, c->B, c->p.bc_y, c->p.collision, c->relax, grid, c->tb_l2,
-                                c->tb_wall_w16, mon, peers ? 1 : 0, c->s);
+                                c->tb_wall_w16, mon, peers ? 1 : 0, inpull ? &pull : nullptr, c->s);
   }));
   if (peers) {  // publish: this launch is complete (the neighbours may now read our new state)
     c->peer_step += 1;
@@ -891,7 +936,8 @@ int lb_sync(lb_ctx* c) {
   if (!c) return fail(LB_EINVAL, "ctx is NULL");
   CU(cudaStreamSynchronize(c->s));
   CU(cudaStreamSynchronize(c->s_comm));
-  return check_peer_status(c);
+  TRY(check_peer_status(c));
+  return check_nonphys(c);
 }
 
 int lb_gather(lb_ctx* c, double* host_out, int root) {
@@ -973,16 +1019,17 @@ static int invariants_enqueue(lb_ctx* c, double* host_dst) {
     const int G = c->mon_tb_G;
     TRY(launch(c, "k_monitor_reduce", c->s, 0, [&] {
       return lbk::launch_monitor_reduce(c->d_mon_tb + (int64_t)G * 5, G, c->d_mon_tb + (int64_t)c->mon_tb_cap * 10,
-                                        c->d_ticket, out, c->s);
+                                        c->d_ticket, out, c->d_nonphys, c->s);
     }));
   } else if (c->mon_valid) {
     const int64_t nslots = (int64_t)lbk::monitor_slots(c->g);
     TRY(launch(c, "k_monitor_reduce", c->s, 0, [&] {
-      return lbk::launch_monitor_reduce(c->d_mon, nslots, c->d_mon + nslots * 5, c->d_ticket, out, c->s);
+      return lbk::launch_monitor_reduce(c->d_mon, nslots, c->d_mon + nslots * 5, c->d_ticket, out, c->d_nonphys,
+                                        c->s);
     }));
   } else {
     TRY(launch(c, "k_invariants", c->s, c->L.sites, [&] {
-      return lbk::launch_invariants(c->g, c->A, c->d_part, out, c->s);
+      return lbk::launch_invariants(c->g, c->A, c->d_part, out, c->d_nonphys, c->s);
     }));
   }
   if (mapped) return LB_OK;
@@ -1024,7 +1071,7 @@ int lb_invariants_pair_async(lb_ctx* c, double* host_out) {
   double* res = c->d_part + lbk::invariants_scratch(c->g);  // 2 x 5 doubles of device result space
   const int G = c->mon_tb_G;
   TRY(launch(c, "k_monitor_reduce_pair", c->s, 0, [&] {
-    return lbk::launch_monitor_reduce_pair(c->d_mon_tb, G, mapped ? mapped : res, c->s);
+    return lbk::launch_monitor_reduce_pair(c->d_mon_tb, G, mapped ? mapped : res, c->d_nonphys, c->s);
   }));
   if (!mapped) CU(cudaMemcpyAsync(host_out, res, 10 * sizeof(double), cudaMemcpyDeviceToHost, c->s));
   return LB_OK;
@@ -1118,6 +1165,10 @@ int lb_set_option(lb_ctx* c, int option, int value) {
     case LB_OPT_TB_WALL_WEIGHT:
       if (value < 1 || value > 256) return fail(LB_EINVAL, "wall weight (x16) must be in [1, 256]");
       c->tb_wall_w16 = value;
+      return LB_OK;
+    case LB_OPT_TB_EDGE_PULL:
+      if (value != 0 && value != 1) return fail(LB_EINVAL, "edge pull must be 0 (k_tb_pull) or 1 (in-kernel)");
+      c->tb_edge_pull = value;
       return LB_OK;
     case LB_OPT_FUSED_IMPL:
       if (value != 0 && value != 1) return fail(LB_EINVAL, "fused impl must be 0 (gather) or 1 (TMA)");

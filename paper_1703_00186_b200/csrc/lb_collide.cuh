@@ -40,8 +40,8 @@ LB_HD constexpr double ipow(int c, int p) {
 // M'_a = (1 - omega) M_a(f) + omega rho m_p(ux, T) m_q(uy, T): the raw moments
 // of f blended with the Maxwellian moments that f_eq reproduces exactly
 // (m_k(u, T) = E[(u + sqrt(T) Z)^k], lattice units).
-// hook(moments): rho, j = (M_10, M_01) and e = M_20 + M_02 of the pre-collision
-// f (monitors, lb_tb.cu; ux, uy, T are not filled).
+// hook(moments): rho, j = (M_10, M_01), e = M_20 + M_02 and u, T of the
+// pre-collision f (monitors and failure detection, lb_tb.cu).
 template <class Hook = NoHook>
 __device__ __forceinline__ void collide_site_reg(double (&f)[Q], const Relax& r, const Hook& hook = Hook{}) {
   const double omega = r.omega, one_m_omega = r.one_m_omega;
@@ -92,17 +92,20 @@ __device__ __forceinline__ void collide_site_reg(double (&f)[Q], const Relax& r,
   }
   // 3. macroscopic fields (Eq. 2): rho, u, T = (e/rho - |u|^2)/2
   const double rho = M[0];
+  const double inv = __drcp_rn(rho);
+  const double ux0 = dmul(M[6], inv), uy0 = dmul(M[9], inv);
+  const double Tm0 = dmul(0.5, dsub(dmul(dadd(M[1], M[2]), inv), dfma(ux0, ux0, dmul(uy0, uy0))));
   {
-    Macro mo;  // ux, uy, T not filled (the hook uses rho, j, e)
+    Macro mo;
     mo.rho = rho;
     mo.jx = M[6];
     mo.jy = M[9];
     mo.e = dadd(M[1], M[2]);
+    mo.ux = ux0;
+    mo.uy = uy0;
+    mo.T = Tm0;
     hook(mo);
   }
-  const double inv = __drcp_rn(rho);
-  const double ux0 = dmul(M[6], inv), uy0 = dmul(M[9], inv);
-  const double Tm0 = dmul(0.5, dsub(dmul(dadd(M[1], M[2]), inv), dfma(ux0, ux0, dmul(uy0, uy0))));
   // equilibrium arguments with the body-force shift (G7b)
   const double ux = dadd(ux0, r.tgx), uy = dadd(uy0, r.tgy), Tm = dadd(Tm0, r.dT);
   // 4. Maxwellian moments per axis

@@ -63,11 +63,13 @@ size_t monitor_slots(const Geo& g);
 // Sum of the slots into out[5] (device or host-mapped pointer) in one launch;
 // part: MON_REDUCE_MAX_BLOCKS x 5 doubles of scratch, ticket: a zeroed counter
 // (left zeroed).  Deterministic: fixed block ranges, partials summed in order.
+// flag (may be null): set to 1 if a result has a NaN sum or min rho <= 0.
 constexpr int MON_REDUCE_MAX_BLOCKS = 148;
 cudaError_t launch_monitor_reduce(const double* mon, int64_t nslots, double* part, unsigned int* ticket,
-                                  double* out, cudaStream_t s);
+                                  double* out, unsigned int* flag, cudaStream_t s);
 // Two slot sets (nslots each, consecutive) reduced by one block into out[10].
-cudaError_t launch_monitor_reduce_pair(const double* mon, int64_t nslots, double* out, cudaStream_t s);
+cudaError_t launch_monitor_reduce_pair(const double* mon, int64_t nslots, double* out, unsigned int* flag,
+                                       cudaStream_t s);
 // TMA-staged kernels (lb_tma.cu): tensor maps of both buffers, built once.
 // Buffer k viewed as {nyp rows, 37 populations, nx columns}, box {256, 1, 1}.
 struct TmaMaps {
@@ -110,15 +112,32 @@ bool tb_layout_ok(int ly);
 void tb_destroy(TbMaps* t);
 // lb_tb.cu's own copies of the wall constants and the Gram inverse
 cudaError_t tb_upload_constants(const double* k_bottom, const double* k_top, const double* ginv, cudaStream_t s);
+// N > 1, in-kernel edge pulls (the default of peer mode): only the CTAs whose
+// sweep reads or writes within 6 columns of a slab edge wait (thread 0,
+// ld.acquire.sys, watchdog) until that neighbour completed as many launches as
+// this rank, then copy the rows of the neighbour's 6 edge columns their strip
+// needs into the staging buffer themselves; every other CTA starts at once,
+// so the exchange overlaps the interior sweeps (§8a6).
+struct TbPeer {
+  const double* L = nullptr;   // left neighbour's current buffer (peer memory)
+  const double* R = nullptr;   // right neighbour's current buffer
+  double* stage = nullptr;     // tb_attach_staging's buffer
+  const unsigned long long* waitL = nullptr;
+  const unsigned long long* waitR = nullptr;
+  const unsigned long long* my_done = nullptr;
+  unsigned int* status = nullptr;
+  unsigned long long timeout_ns = 0;
+};
 // grid: CTAs (one per SM); l2_dist: L2 prefetch distance in columns (0 = off; LSU prefetch);
 // wall_w16: cost of a wall-strip column in 1/16 of an interior one (work split);
 // mon != nullptr: monitors, 2 x tb_grid(g, grid) x 5 doubles of per-CTA
 // partials (state n+1, then state n+2)
 // peers != 0: columns beyond the slab come from the staging buffer (N > 1) and
 // B's halo is not written; else the N = 1 periodic wrap.
+// pull != nullptr (peers only): in-kernel edge pulls instead of a preceding launch_tb_pull.
 cudaError_t launch_step2_tb(const Geo& g, const TbMaps* t, int src_buf, double* B, int bc, int coll,
                             const lbd::Relax& r, int grid, int l2_dist, int wall_w16, double* mon, int peers,
-                            cudaStream_t s);
+                            const TbPeer* pull, cudaStream_t s);
 // CTAs a two-step launch with `grid` requested actually uses
 int tb_grid(const Geo& g, int grid);
 // this rank's counter += 1 (system-scope release), after the step kernel
@@ -136,6 +155,6 @@ cudaError_t launch_internal_to_canon(const Geo& g, const double* A, double* cano
 // partials: scratch of at least invariants_scratch(g) doubles; out: 5 doubles on device
 size_t invariants_scratch(const Geo& g);
 cudaError_t launch_invariants(const Geo& g, const double* A, double* partials, double* out,
-                              cudaStream_t s);
+                              unsigned int* flag, cudaStream_t s);
 
 }  // namespace lbk

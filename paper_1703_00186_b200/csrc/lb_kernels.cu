@@ -554,6 +554,15 @@ cudaError_t launch_internal_to_canon(const Geo& g, const double* A, double* cano
 // E = 1/2 sum |c|^2 f, and min rho.
 constexpr int RED_TPB = 256;
 
+// Failure detection ("numerical blow-up"): a final
+// invariants result with a NaN sum or min rho <= 0 (NaN densities arrive as
+// -inf) sets the context's sticky device flag, which lb_sync reports as
+// LB_ENONPHYS — so the asynchronous monitored path needs no host-side check.
+__device__ __forceinline__ void flag_nonphysical(const double (&v)[5], unsigned int* flag) {
+  const bool bad = v[0] != v[0] || v[1] != v[1] || v[2] != v[2] || v[3] != v[3] || !(v[4] > 0.0);
+  if (bad && flag) atomicOr(flag, 1u);
+}
+
 __device__ __forceinline__ void block_reduce5(double (&v)[5], double* sm) {
   const int t = threadIdx.x;
 #pragma unroll
@@ -601,7 +610,8 @@ __global__ void __launch_bounds__(RED_TPB) k_invariants_partial(const double* __
 }
 
 __global__ void __launch_bounds__(RED_TPB) k_invariants_final(const double* __restrict__ part,
-                                                              int nb, double* __restrict__ out) {
+                                                              int nb, double* __restrict__ out,
+                                                              unsigned int* flag) {
   __shared__ double sm[5 * RED_TPB];
   double v[5] = {0.0, 0.0, 0.0, 0.0, INFINITY};
   for (int b = threadIdx.x; b < nb; b += RED_TPB) {
@@ -611,19 +621,21 @@ __global__ void __launch_bounds__(RED_TPB) k_invariants_final(const double* __re
     v[4] = (m != m || m == -INFINITY) ? -INFINITY : fmin(v[4], m);
   }
   block_reduce5(v, sm);
-  if (threadIdx.x == 0)
+  if (threadIdx.x == 0) {
 #pragma unroll
     for (int k = 0; k < 5; ++k) out[k] = v[k];
+    flag_nonphysical(v, flag);
+  }
 }
 
 size_t invariants_scratch(const Geo& g) { return (size_t)g.lx * 5; }
 
 cudaError_t launch_invariants(const Geo& g, const double* A, double* partials, double* out,
-                              cudaStream_t s) {
+                              unsigned int* flag, cudaStream_t s) {
   k_invariants_partial<<<g.lx, RED_TPB, 0, s>>>(A, g, partials);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  k_invariants_final<<<1, RED_TPB, 0, s>>>(partials, g.lx, out);
+  k_invariants_final<<<1, RED_TPB, 0, s>>>(partials, g.lx, out, flag);
   return cudaGetLastError();
 }
 
@@ -634,7 +646,7 @@ cudaError_t launch_invariants(const Geo& g, const double* A, double* partials, d
 // (a one-block pass over 30k slots cost 56 us per step).
 __global__ void __launch_bounds__(RED_TPB) k_monitor_reduce(const double* __restrict__ mon, int nslots,
                                                             double* part, unsigned int* ticket,
-                                                            double* out) {
+                                                            double* out, unsigned int* flag) {
   __shared__ double sm[5 * RED_TPB];
   __shared__ bool last;
   const int t = threadIdx.x;
@@ -669,6 +681,7 @@ __global__ void __launch_bounds__(RED_TPB) k_monitor_reduce(const double* __rest
   if (t == 0) {
 #pragma unroll
     for (int k = 0; k < 5; ++k) out[k] = w[k];
+    flag_nonphysical(w, flag);
     *ticket = 0u;  // ready for the next launch (stream-ordered)
   }
 }
@@ -676,7 +689,7 @@ __global__ void __launch_bounds__(RED_TPB) k_monitor_reduce(const double* __rest
 // Both states of a two-step launch in ONE single-block launch (nslots per
 // set, set 1 at mon + 5 nslots): out[0..4] = set 0, out[5..9] = set 1.
 __global__ void __launch_bounds__(RED_TPB) k_monitor_reduce_pair(const double* __restrict__ mon, int nslots,
-                                                                 double* out) {
+                                                                 double* out, unsigned int* flag) {
   __shared__ double sm[5 * RED_TPB];
   const int t = threadIdx.x;
   for (int set = 0; set < 2; ++set) {
@@ -689,15 +702,18 @@ __global__ void __launch_bounds__(RED_TPB) k_monitor_reduce_pair(const double* _
       v[4] = (m != m || m == -INFINITY) ? -INFINITY : fmin(v[4], m);
     }
     block_reduce5(v, sm);
-    if (t == 0)
+    if (t == 0) {
 #pragma unroll
       for (int k = 0; k < 5; ++k) out[set * 5 + k] = v[k];
+      flag_nonphysical(v, flag);
+    }
     __syncthreads();  // sm reused
   }
 }
 
-cudaError_t launch_monitor_reduce_pair(const double* mon, int64_t nslots, double* out, cudaStream_t s) {
-  k_monitor_reduce_pair<<<1, RED_TPB, 0, s>>>(mon, (int)nslots, out);
+cudaError_t launch_monitor_reduce_pair(const double* mon, int64_t nslots, double* out, unsigned int* flag,
+                                       cudaStream_t s) {
+  k_monitor_reduce_pair<<<1, RED_TPB, 0, s>>>(mon, (int)nslots, out, flag);
   return cudaGetLastError();
 }
 
@@ -707,8 +723,8 @@ static int monitor_reduce_blocks(int64_t nslots) {
 }
 
 cudaError_t launch_monitor_reduce(const double* mon, int64_t nslots, double* part, unsigned int* ticket,
-                                  double* out, cudaStream_t s) {
-  k_monitor_reduce<<<monitor_reduce_blocks(nslots), RED_TPB, 0, s>>>(mon, (int)nslots, part, ticket, out);
+                                  double* out, unsigned int* flag, cudaStream_t s) {
+  k_monitor_reduce<<<monitor_reduce_blocks(nslots), RED_TPB, 0, s>>>(mon, (int)nslots, part, ticket, out, flag);
   return cudaGetLastError();
 }
 

@@ -248,6 +248,17 @@ constexpr bool vrows_ok() {
 // FP64 operations per site instead of a second pass over the 37 values (the
 // two-step kernel is FP64-latency-bound).  They equal the sums over the stored
 // state up to rounding (tests: <= 1e-13 of the mass).
+//
+// Failure detection: the minimum takes -inf when this collision's own output
+// cannot be finite — rho NaN, or u or T NaN / infinite (f_eq and the relaxed
+// values are then NaN; 0 * inf = NaN below) — so a blow-up created by the
+// collision that produces the stored state is flagged by the same launch
+// (k_monitor_reduce* -> the context's non-physical flag -> LB_ENONPHYS at lb_sync).
+__device__ __forceinline__ double checked_rho(const Macro& m) {
+  const double chk = __fma_rn(0.0, __dadd_rn(__dadd_rn(m.ux, m.uy), m.T), m.rho);
+  return chk != chk ? -INFINITY : m.rho;
+}
+
 __device__ __forceinline__ void acc_invariants(const Macro& m, const Relax& r, double (&a)[5]) {
   if (r.tgx == 0.0 && r.tgy == 0.0 && r.dT == 0.0) {
     // no body force (uniform branch): the increments below are exact zeros
@@ -255,7 +266,7 @@ __device__ __forceinline__ void acc_invariants(const Macro& m, const Relax& r, d
     a[1] = __dadd_rn(a[1], m.jx);
     a[2] = __dadd_rn(a[2], m.jy);
     a[3] = __dadd_rn(a[3], __dmul_rn(0.5, m.e));
-    a[4] = fmin(a[4], m.rho != m.rho ? -INFINITY : m.rho);
+    a[4] = fmin(a[4], checked_rho(m));
     return;
   }
   const double djx = __dmul_rn(r.omega, __dmul_rn(m.rho, r.tgx));
@@ -267,7 +278,24 @@ __device__ __forceinline__ void acc_invariants(const Macro& m, const Relax& r, d
   a[1] = __dadd_rn(a[1], __dadd_rn(m.jx, djx));
   a[2] = __dadd_rn(a[2], __dadd_rn(m.jy, djy));
   a[3] = __dadd_rn(a[3], __fma_rn(0.5, m.e, dE));
-  a[4] = fmin(a[4], m.rho != m.rho ? -INFINITY : m.rho);
+  a[4] = fmin(a[4], checked_rho(m));
+}
+
+#ifndef LB_TB_FAKE
+#define LB_TB_FAKE 0
+#endif
+// The collision of both phases.  LB_TB_FAKE (variant builds only, timing
+// experiments): a one-multiply stand-in, to time the kernel's data-movement
+// skeleton without the FP64 work (results are then meaningless).
+template <int COLL, class Hook>
+__device__ __forceinline__ void tb_collide(double (&f)[Q], const Relax& r, const Hook& hook) {
+#if LB_TB_FAKE
+#pragma unroll
+  for (int l = 0; l < Q; ++l) f[l] = __dmul_rn(f[l], r.one_m_omega);
+#else
+  if (COLL == COLL_REGULARIZED) collide_site_reg(f, r, hook);
+  else collide_site(f, r, hook);
+#endif
 }
 
 // Phase 1 site update: state n+1 at row y = ya - 3 + i from state-n buffer b
@@ -282,18 +310,22 @@ __device__ __forceinline__ void phase1_gather(const double* s0, int b, int i, do
   for (int l = 0; l < Q; ++l) f[l] = sb[POFF(l, RB) + 3 - CY(l)];
 }
 
-template <int COLL, int R1, bool MON>
-__device__ __forceinline__ void phase1_update(double (&f)[Q], double* s1, int t, int i, int y, int ly,
-                                              bool thermal, const Relax& r, bool own, double (&acc)[5]) {
-  const int io = opaque(i);
-  const bool wall = y < 3 || y >= ly - 3;
-  if (thermal && wall) thermal_wall(f, y < 3 ? 0 : 1);
+template <int COLL, bool MON>
+__device__ __forceinline__ void phase1_collide(double (&f)[Q], int y, int ly, bool thermal, const Relax& r, bool own,
+                                               double (&acc)[5]) {
+  if (thermal && (y < 3 || y >= ly - 3)) thermal_wall(f, y < 3 ? 0 : 1);
   // monitors: accumulated as soon as the collision has formed the moments
   auto hook = [&](const Macro& m) {
     if (MON && own) acc_invariants(m, r, acc);
   };
-  if (COLL == COLL_REGULARIZED) collide_site_reg(f, r, hook);
-  else collide_site(f, r, hook);
+  tb_collide<COLL>(f, r, hook);
+}
+
+// state n+1 of row y into the ring slot of iteration t (+ the virtual rows it mirrors into)
+template <int R1>
+__device__ __forceinline__ void phase1_store(const double (&f)[Q], double* s1, int t, int i, int y, int ly) {
+  const int io = opaque(i);
+  const bool wall = y < 3 || y >= ly - 3;
 #pragma unroll
   for (int l = 0; l < Q; ++l) s1[(SLOTS1_BEFORE(l) + (t % L1(l))) * R1 + io] = f[l];
   if (wall) {
@@ -305,6 +337,13 @@ __device__ __forceinline__ void phase1_update(double (&f)[Q], double* s1, int t,
       for (int l = 0; l < Q; ++l) s1[(SLOTS1_BEFORE(REFL(l)) + (t % L1(l))) * R1 + vi] = f[l];
     }
   }
+}
+
+template <int COLL, int R1, bool MON>
+__device__ __forceinline__ void phase1_update(double (&f)[Q], double* s1, int t, int i, int y, int ly,
+                                              bool thermal, const Relax& r, bool own, double (&acc)[5]) {
+  phase1_collide<COLL, MON>(f, y, ly, thermal, r, own, acc);
+  phase1_store<R1>(f, s1, t, i, y, ly);
 }
 
 // Phase 2 site update: state n+2 at row y = ya + i, column c2, from the
@@ -333,8 +372,7 @@ __device__ __forceinline__ void phase2_update(double (&f)[Q], double* __restrict
   auto hook = [&](const Macro& m) {
     if (MON && own) acc_invariants(m, r, acc);
   };
-  if (COLL == COLL_REGULARIZED) collide_site_reg(f, r, hook);
-  else collide_site(f, r, hook);
+  tb_collide<COLL>(f, r, hook);
   // 64-bit stride: one IMAD.WIDE per store instead of IMAD + LEA + LEA.HI.X
   const int64_t nyp = opaque(g.nyp);
   double* p = B + (int64_t)c2 * g.cs + g.y0 + y;
@@ -380,6 +418,12 @@ __device__ __forceinline__ void phase2(const double* s1, double* __restrict__ B,
 #ifndef LB_TB_DECOUPLE
 #define LB_TB_DECOUPLE 2
 #endif
+// bit 0: BGK, bit 1: regularised — the kernels NOT decoupled with mbarriers
+// hand the ring over with two hardware named barriers (producer bar.arrive,
+// consumer bar.sync) instead of one CTA barrier per iteration
+#ifndef LB_TB_NBAR
+#define LB_TB_NBAR 0
+#endif
 constexpr int TB_HT = LB_TB_HT;
 constexpr int TB_PF = LB_TB_PF;
 using Cfg = TbCfg<TB_HT, TB_PF>;
@@ -406,11 +450,52 @@ struct alignas(64) TbKMaps {
 // of its strips not covered by a lower strip, its output columns) for state
 // n+1 into mon[blockIdx] and for state n+2 into mon[gridDim + blockIdx]
 // (5 doubles each; fixed-order reductions, deterministic).
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Thread 0 waits until the neighbour counters that are non-null reach *my_done
+// (watchdog: *status = 1 after timeout_ns, then proceed; LB_EPEER at the next sync).
+__device__ __forceinline__ void peer_wait(const unsigned long long* a, const unsigned long long* b,
+                                          const unsigned long long* my_done, unsigned int* status,
+                                          unsigned long long timeout_ns) {
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  const unsigned long long want = *my_done;
+  while ((a && ld_acquire_sys_u64(a) < want) || (b && ld_acquire_sys_u64(b) < want)) {
+    __nanosleep(128);
+    unsigned long long t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    if (timeout_ns && t1 - t0 > timeout_ns) {
+      atomicExch(status, 1u);
+      break;
+    }
+  }
+}
+
+// Rows [r0, r0 + RB) of the 6 staged columns of one side (all 37 populations),
+// clipped to the nyp rows of a population column (the TMA box zero-fills rows
+// beyond it): src = the neighbour's first staged column, dst = that side's
+// staging block.  r0 and nyp are even: 16-byte moves.
+template <int RB, int NT>
+__device__ __forceinline__ void edge_copy(double* __restrict__ dst, const double* src, int64_t cs, int nyp, int r0) {
+  const int n2 = (min(RB, nyp - r0)) / 2;  // double2 per population column
+  const int per_col = Q * n2;
+  for (int q = threadIdx.x; q < 6 * per_col; q += NT) {
+    const int col = q / per_col, rem = q - col * per_col;
+    const int l = rem / n2, k = rem - l * n2;
+    const int64_t off = col * cs + (int64_t)l * nyp + r0 + 2 * k;
+    *reinterpret_cast<double2*>(dst + off) = __ldcg(reinterpret_cast<const double2*>(src + off));
+  }
+}
+
 template <int COLL, int HT, int PF, bool MON>
 __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
     k_step2_tb(const __grid_constant__ TbKMaps km, double* __restrict__ B, Geo g, Relax r, int nstrips,
                int l2_dist, int thermal, int wall_w16, double* __restrict__ mon, int peers,
-               const double* __restrict__ Asrc) {
+               const double* __restrict__ Asrc, TbPeer pp, int inpull) {
   using C = TbCfg<HT, PF>;
   constexpr int RB = C::RB, BUFD = C::BUFD, R1 = C::R1, NB = C::NB;
   // EARLY (LB_TB_EARLY, or PF = 0): the phase-1 warps refill the buffer they
@@ -426,6 +511,18 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
   // can run up to one iteration ahead of the other.
   constexpr bool DECOUPLE = (LB_TB_DECOUPLE >> (COLL == COLL_REGULARIZED ? 1 : 0)) & 1;
   static_assert(!DECOUPLE || EARLY, "decoupled phases need the phase-1 warps to issue the loads");
+  // NBAR: named barriers F(t) = 3 + (t & 1), "phase 1 wrote iteration t"
+  // (phase 1 arrives, phase 2 syncs before its gather of t + 1), and
+  // E(t) = 5 + (t & 1), "phase 2 gathered iteration t" (phase 2 arrives,
+  // phase 1 syncs before its ring stores of t + 1, which overwrite the slots
+  // phase 2 read in t).  Each phase can run up to one iteration ahead; the
+  // two ids per direction keep a barrier's next arrival behind the
+  // completion of its previous generation (hardware barriers count
+  // arrivals: a second arrival of the same side would complete it alone).
+  // Arrivals (t = 0 .. niter - 2) and syncs (t = 1 .. niter - 1) pair up
+  // within a sweep, so no generation is left open across sweeps.
+  constexpr bool NBAR = !DECOUPLE && ((LB_TB_NBAR >> (COLL == COLL_REGULARIZED ? 1 : 0)) & 1);
+  static_assert(!NBAR || EARLY, "named-barrier hand-over needs the phase-1 warps to issue the loads");
   extern __shared__ __align__(128) double sm[];
   double* s0 = sm;
   double* s1 = sm + C::S0_DBL;
@@ -487,6 +584,26 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
     const bool vbottom = ya - 3 < 3;
     const bool vtop = ya + HT + 3 > ly - 3;
 
+    // N > 1, in-kernel edge pulls: this sweep reads state-n columns [x0 - 6,
+    // x1 + 6) and writes [x0, x1).  Within 6 columns of the left edge it reads
+    // the left neighbour's last columns (complete once its previous launch
+    // is) and overwrites columns the neighbour's previous launch pulled: wait
+    // for its counter, then stage this strip's rows of its 6 edge columns.
+    // Same on the right.  Interior sweeps never wait.
+    if (inpull) {
+      const bool needL = x0 < 6, needR = x1 > lx - 6;
+      if (needL || needR) {  // CTA-uniform
+        if (tid == 0) peer_wait(needL ? pp.waitL : nullptr, needR ? pp.waitR : nullptr, pp.my_done, pp.status,
+                                pp.timeout_ns);
+        __syncthreads();
+        if (needL) edge_copy<RB, C::NT>(pp.stage, pp.L + (int64_t)(lx - 3) * g.cs, g.cs, g.nyp, rbase - 6);
+        if (needR) edge_copy<RB, C::NT>(pp.stage + 6 * g.cs, pp.R + 3 * g.cs, g.cs, g.nyp, rbase - 6);
+        // generic-proxy global writes, read next by this CTA's TMA (async proxy)
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        __syncthreads();
+      }
+    }
+
     // TMA of the state-n window of column group g that phase 1 of iteration k
     // pulls (column c1(k) - cx_g, rows [ya - 6, ya + HT + 6)); one thread per
     // group; the thread of g = 0 also posts the expected bytes (complete_tx may
@@ -529,7 +646,7 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
 
     for (int t = 0; t < niter; ++t) {
       const uint32_t I = iglob + (uint32_t)t;
-      if (!DECOUPLE) __syncthreads();  // every read of iteration t-1 is done: the buffers refilled below are free
+      if (!DECOUPLE && !NBAR) __syncthreads();  // every read of iteration t-1 is done: the buffers refilled below are free
       if (l2_dist > 0 && t + l2_dist < nload) {
         // L2 prefetch (LSU, not the TMA queue) of the newest column the loads
         // of iteration t + l2_dist touch: rows [ya - 6, ya + HT + 6) of all 37
@@ -580,13 +697,33 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
             phase1_gather<BUFD, RB>(s0, buf, valid ? i : 0, f);
             asm volatile("bar.sync 2, %0;" ::"r"(32 * C::NW1) : "memory");
             if (issuer && t + NB < nload) issue_one(t + NB, my_grp);
-            if (valid) phase1_update<COLL, R1, MON>(f, s1, t, i, y, ly, thermal, r, own, acc);
+            if (NBAR) {
+              if (valid) phase1_collide<COLL, MON>(f, y, ly, thermal, r, own, acc);
+              if (t > 0) asm volatile("bar.sync %0, %1;" ::"r"(5 + ((t - 1) & 1)), "r"(C::NT) : "memory");
+              if (valid) phase1_store<R1>(f, s1, t, i, y, ly);
+            } else if (valid) {
+              phase1_update<COLL, R1, MON>(f, s1, t, i, y, ly, thermal, r, own, acc);
+            }
           } else if (valid) {
             phase1<COLL, BUFD, RB, R1, MON>(s0, s1, buf, t, i, y, ly, thermal, r, own, acc);
           }
         }
+        else if (NBAR && t > 0)  // t >= nload: no stores, but the hand-over protocol continues
+          asm volatile("bar.sync %0, %1;" ::"r"(5 + ((t - 1) & 1)), "r"(C::NT) : "memory");
         if (DECOUPLE)  // item I written (every phase-1 thread arrives: release of its ring stores)
           asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar_full + 8 * (I & 1)) : "memory");
+        if (NBAR && t + 1 < niter) asm volatile("bar.arrive %0, %1;" ::"r"(3 + (t & 1)), "r"(C::NT) : "memory");
+      } else if (NBAR) {
+        // phase 2 (named-barrier hand-over): wait until phase 1 wrote t - 1, gather, release
+        if (t > 0) asm volatile("bar.sync %0, %1;" ::"r"(3 + ((t - 1) & 1)), "r"(C::NT) : "memory");
+        const int i = tid - 32 * C::NW1;
+        const int y = ya + i;
+        const bool valid = t >= 7 && i < HT && y < ly;
+        double f[Q];
+        if (t >= 7) phase2_gather<R1>(s1, t, valid ? i : 0, f);
+        if (t + 1 < niter) asm volatile("bar.arrive %0, %1;" ::"r"(5 + (t & 1)), "r"(C::NT) : "memory");
+        if (valid)
+          phase2_update<COLL, MON>(f, B, g, y, xs - 7 + t, thermal, r, y >= own_lo && y < own_hi, acc, !peers);
       } else if (DECOUPLE) {
         // phase 2 (decoupled): wait for item I - 1, gather, release the slots
         if (t > 0) mbar_wait(bar_full + 8 * ((I - 1) & 1), ((I - 1) >> 1) & 1);
@@ -678,7 +815,8 @@ bool encode(CUtensorMap* m, double* base, const Geo& g, int box_rows, int box_po
 
 template <int COLL, bool MON>
 cudaError_t launch_tb(const Geo& g, const TbMaps* t, int src_buf, double* B, const Relax& r, int grid,
-                      int l2_dist, int thermal, int wall_w16, double* mon, int peers, cudaStream_t s) {
+                      int l2_dist, int thermal, int wall_w16, double* mon, int peers, const TbPeer* pull,
+                      cudaStream_t s) {
   auto kern = k_step2_tb<COLL, TB_HT, TB_PF, MON>;
   static unsigned long long done_mask = 0;  // opt-in smem is a per-device attribute
   int dev = 0;
@@ -696,8 +834,10 @@ cudaError_t launch_tb(const Geo& g, const TbMaps* t, int src_buf, double* B, con
     km.stL[c] = peers ? t->st[0][c] : t->load[src_buf][c];
     km.stR[c] = peers ? t->st[1][c] : t->load[src_buf][c];
   }
+  const TbPeer pp = (peers && pull) ? *pull : TbPeer{};
   kern<<<tb_grid(g, grid), Cfg::NT, Cfg::SMEM, s>>>(km, B, g, r, (g.ly + TB_HT - 1) / TB_HT, l2_dist, thermal,
-                                                    wall_w16, mon, peers, t->bufs[src_buf]);
+                                                    wall_w16, mon, peers, t->bufs[src_buf], pp,
+                                                    (peers && pull) ? 1 : 0);
   return cudaGetLastError();
 }
 
@@ -752,26 +892,20 @@ cudaError_t tb_upload_constants(const double* k_bottom, const double* k_top, con
 
 cudaError_t launch_step2_tb(const Geo& g, const TbMaps* t, int src_buf, double* B, int bc, int coll,
                             const Relax& r, int grid, int l2_dist, int wall_w16, double* mon, int peers,
-                            cudaStream_t s) {
+                            const TbPeer* pull, cudaStream_t s) {
   if (bc != BC_THERMAL && bc != BC_ADIABATIC) return cudaErrorNotSupported;
   const int th = bc == BC_THERMAL;
   if (mon)
     return coll == COLL_REGULARIZED
-               ? launch_tb<COLL_REGULARIZED, true>(g, t, src_buf, B, r, grid, l2_dist, th, wall_w16, mon, peers, s)
-               : launch_tb<COLL_BGK, true>(g, t, src_buf, B, r, grid, l2_dist, th, wall_w16, mon, peers, s);
+               ? launch_tb<COLL_REGULARIZED, true>(g, t, src_buf, B, r, grid, l2_dist, th, wall_w16, mon, peers, pull, s)
+               : launch_tb<COLL_BGK, true>(g, t, src_buf, B, r, grid, l2_dist, th, wall_w16, mon, peers, pull, s);
   return coll == COLL_REGULARIZED
-             ? launch_tb<COLL_REGULARIZED, false>(g, t, src_buf, B, r, grid, l2_dist, th, wall_w16, mon, peers, s)
-             : launch_tb<COLL_BGK, false>(g, t, src_buf, B, r, grid, l2_dist, th, wall_w16, mon, peers, s);
+             ? launch_tb<COLL_REGULARIZED, false>(g, t, src_buf, B, r, grid, l2_dist, th, wall_w16, mon, peers, pull, s)
+             : launch_tb<COLL_BGK, false>(g, t, src_buf, B, r, grid, l2_dist, th, wall_w16, mon, peers, pull, s);
 }
 
 // ---- N > 1: staging of the neighbours' edge columns (peer memory -> local)
 namespace {
-
-__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
 
 // Every block's thread 0 waits until both neighbours completed as many launches
 // as this rank (their current buffer then holds the same state as ours, and
@@ -781,20 +915,7 @@ __global__ void __launch_bounds__(256) k_tb_pull(double2* __restrict__ stage, co
                                                  int64_t lx, int64_t cs2, const unsigned long long* waitL,
                                                  const unsigned long long* waitR, const unsigned long long* my_done,
                                                  unsigned int* status, unsigned long long timeout_ns) {
-  if (threadIdx.x == 0) {
-    unsigned long long t0;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    const unsigned long long want = *my_done;
-    while (ld_acquire_sys_u64(waitL) < want || ld_acquire_sys_u64(waitR) < want) {
-      __nanosleep(128);
-      unsigned long long t1;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-      if (timeout_ns && t1 - t0 > timeout_ns) {
-        atomicExch(status, 1u);
-        break;
-      }
-    }
-  }
+  if (threadIdx.x == 0) peer_wait(waitL, waitR, my_done, status, timeout_ns);
   __syncthreads();
   const int64_t n = 6 * cs2;  // double2 per side
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 2 * n; i += (int64_t)gridDim.x * blockDim.x)

@@ -432,11 +432,13 @@ class Lattice:
         _check(lib().lb_set_peers(self._ctx, ctypes.byref(P)))
 
     def set_propagate_impl(self, impl: str):
-        """'ldg' (default) or 'tma' (TMA-staged windows) for lb_propagate."""
+        """'tma' (TMA-staged windows; the library default when the tensor maps
+        encode, lb_init) or 'ldg' (register gather) for lb_propagate."""
         _check(lib().lb_set_option(self._ctx, 0, {"ldg": 0, "tma": 1}[impl]))
 
     def set_fused_impl(self, impl: str):
-        """'ldg' (default) or 'tma' for the fused step kernel (N=1, walls)."""
+        """'ldg' (register gather, the default) or 'tma' (TMA-staged windows)
+        for the one-step fused kernel (N=1, walls, monitors off)."""
         _check(lib().lb_set_option(self._ctx, 1, {"ldg": 0, "tma": 1}[impl]))
 
     def use_graphs(self, enable: bool = True):
@@ -446,7 +448,8 @@ class Lattice:
     def temporal(self, enable: bool = True, grid: int = 0, l2_prefetch: int = 0, wall_weight16: int = 20,
                  l2_promotion: int | None = None):
         """Two steps per pass over HBM (LB_OPT_TEMPORAL, the default where it
-        applies: N = 1, walls, fused mode, monitors off):
+        applies: fused mode, walls, N = 1 or N > 1 in peer mode, monitors on or
+        off — with monitors the kernel reduces both states' invariants):
         lb_step advances pairs of steps with the two-step kernel.  grid: CTAs
         (0 = one per SM); l2_prefetch: L2 prefetch distance in columns (0 = off);
         wall_weight16: cost of a wall-strip column, x16, for the work split;
@@ -457,6 +460,11 @@ class Lattice:
         _check(lib().lb_set_option(self._ctx, 6, int(wall_weight16)))
         if l2_promotion is not None:
             _check(lib().lb_set_option(self._ctx, 7, int(l2_promotion)))
+
+    def edge_pull(self, in_kernel: bool = True):
+        """N > 1 two-step exchange: inside the kernel (edge CTAs wait and stage,
+        the default) or a separate k_tb_pull launch first (LB_OPT_TB_EDGE_PULL)."""
+        _check(lib().lb_set_option(self._ctx, 8, int(bool(in_kernel))))
 
     def monitor(self, enable: bool = True):
         """Fused monitors: invariants reduced inside the step kernel (lb_monitor)."""

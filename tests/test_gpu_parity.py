@@ -34,10 +34,15 @@ def lb():
 
 
 def pair(lb, lx, ly, bc="thermal", mode="fused", overlap=False, tau=0.8, tb=None, tt=None):
+    """(library lattice, oracle lattice).  overlap=True runs the library through
+    an NCCL 1-rank self-ring: the only N = 1 configuration in which the
+    bulk || exchange, then borders schedule (§8a6) exists — lb_init rejects
+    overlap where it would have no effect."""
     T0 = oracle.t0()
     tb = 1.05 * T0 if tb is None else tb
     tt = 0.95 * T0 if tt is None else tt
-    g = lb.Lattice(lx, ly, tau=tau, t_bottom=tb, t_top=tt, bc_y=bc, mode=mode, overlap=overlap)
+    g = lb.Lattice(lx, ly, tau=tau, t_bottom=tb, t_top=tt, bc_y=bc, mode=mode, overlap=overlap,
+                   nccl_id=lb.nccl_unique_id() if overlap else None)
     o = oracle.Lattice(lx, ly, tau=tau, t_bottom=tb, t_top=tt, bc_y=BCN[bc])
     return g, o
 
@@ -126,7 +131,10 @@ def test_collide_parity(lb, tau):
 def test_trajectory_64x32_10_steps(lb, mode, overlap, stride, bc):
     """Config #1: 64x32, RT init on each side, 10 steps, compared after every step
     (stride 1: the one-step kernels) or every second step (stride 2, fused: the
-    two-step kernel, the default for walls at N = 1)."""
+    two-step kernel, the default for walls at N = 1).  overlap: the NCCL
+    self-ring's overlapped schedule (walls only: periodic Y has no overlap)."""
+    if overlap and bc == "periodic":
+        pytest.skip("periodic Y: the y-halo wrap rewrites rows the bulk reads; overlap is rejected")
     lx, ly = 64, 32
     g, o = pair(lb, lx, ly, bc=bc, mode=mode, overlap=overlap)
     fields = lbgen.rt_macro(lx, ly, oracle.t0())
@@ -164,13 +172,27 @@ def test_split_fused_overlap_bit_identical(lb, bc):
     lx, ly = 70, 129
     st = oracle_state(lx, ly, seed=9)
     outs = []
-    for mode, ov in [("split", False), ("fused", False), ("fused", True)]:
-        g = lb.Lattice(lx, ly, bc_y=bc, mode=mode, overlap=ov)
+    arms = [("split", False), ("fused", False)] + ([("fused", True)] if bc != "periodic" else [])
+    for mode, ov in arms:
+        # overlap: the NCCL self-ring (bulk || exchange on the comm stream, then borders)
+        g = lb.Lattice(lx, ly, bc_y=bc, mode=mode, overlap=ov, nccl_id=lb.nccl_unique_id() if ov else None)
         g.set_state(st)
         g.step(7)
         outs.append(g.gather())
-    assert np.array_equal(outs[0], outs[1])
-    assert np.array_equal(outs[1], outs[2])
+        g.close()
+    for o in outs[1:]:
+        assert np.array_equal(outs[0], o)
+
+
+def test_overlap_without_effect_is_rejected(lb):
+    """lb_init returns LB_EINVAL for overlap=1 where the overlapped schedule
+    cannot run (N = 1 without a communicator, split mode, periodic Y), so no
+    configuration can claim an overlap it does not perform."""
+    for kw in ({}, {"mode": "split", "nccl": True}, {"bc_y": "periodic", "nccl": True}):
+        nccl = kw.pop("nccl", False)
+        with pytest.raises(lb.LBError) as ei:
+            lb.Lattice(40, 32, overlap=True, nccl_id=lb.nccl_unique_id() if nccl else None, **kw)
+        assert ei.value.status == 1, kw
 
 
 def test_uniform_wall_equilibrium_fixed_point(lb):
@@ -253,7 +275,7 @@ def test_full_size_1920x2048_one_step(lb, overlap):
     """Config #2 lattice in the launch configuration bench.py times (fused)."""
     lx, ly = 1920, 2048
     fields = lbgen.rt_macro(lx, ly, oracle.t0())
-    g = lb.Lattice(lx, ly, mode="fused", overlap=overlap)
+    g = lb.Lattice(lx, ly, mode="fused", overlap=overlap, nccl_id=lb.nccl_unique_id() if overlap else None)
     g.init_macro(*fields)
     g.step(2)
     got = g.gather()
@@ -286,24 +308,34 @@ def test_full_size_1920x2048_regularized_gravity_split():
 # ------------------------------------------------------------------ NCCL transport on one GPU
 
 @pytest.mark.parametrize("bc,mode,overlap", [("thermal", "fused", True), ("thermal", "fused", False),
-                                             ("thermal", "split", False), ("periodic", "fused", True),
+                                             ("thermal", "split", False), ("periodic", "fused", False),
                                              ("adiabatic", "fused", True)])
 def test_nccl_self_ring_equals_local_wrap(lb, bc, mode, overlap):
     """N = 1 with an NCCL communicator: the exchange runs the N > 1 code path
     (grouped ncclSend/ncclRecv of the contiguous 3-column blocks on the comm
-    stream, bulk || exchange, borders after the event) as a 1-rank ring; it
-    must be bit-identical to the local wrap, and invariants go through
-    ncclAllReduce."""
+    stream; with overlap the bulk columns run while it is in flight and the
+    3+3 border columns after its event) as a 1-rank ring.  It must equal the
+    oracle (<= 1e-12) and the local wrap bit for bit, and invariants go
+    through ncclAllReduce."""
     lx, ly = 40, 70
     st = oracle_state(lx, ly, seed=31)
-    ref = lb.Lattice(lx, ly, bc_y=bc, mode=mode)
+    ref = lb.Lattice(lx, ly, bc_y=bc, mode=mode, temporal=False)
     ref.set_state(st)
     ref.step(6)
     want = ref.gather()
     g = lb.Lattice(lx, ly, bc_y=bc, mode=mode, overlap=overlap, nccl_id=lb.nccl_unique_id())
+    g.profile(True)
     g.set_state(st)
     g.step(6)
-    assert np.array_equal(g.gather(), want)
+    got = g.gather()
+    names = g.profile_read()
+    if overlap:   # the schedule really ran: bulk and border launches, every step
+        assert names["k_step_fused_bulk"]["launches"] == 6 and names["k_step_fused_border"]["launches"] == 6, names
+    assert np.array_equal(got, want)
+    o = oracle.Lattice(lx, ly, bc_y=BCN[bc])
+    o.set_state(st)
+    o.step(6)
+    assert max_rel(got, o.get_state(0)) < TOL
     assert np.allclose(g.invariants(), ref.invariants(), rtol=1e-15, atol=0)
     g.close()
 
@@ -398,19 +430,22 @@ def test_peer_exchange_ring_equals_single_lattice(lb, nranks, streams, coll):
         g.close()
 
 
-@pytest.mark.parametrize("nranks,ly,stride,nsteps", [(2, 70, 2, 9), (3, 150, 2, 6), (4, 230, 2, 7), (2, 40, 3, 9)])
+@pytest.mark.parametrize("nranks,ly,stride,nsteps,lx", [(2, 70, 2, 9, 24), (3, 150, 2, 6, 24), (4, 230, 2, 7, 24),
+                                                        (2, 40, 3, 9, 24), (3, 300, 2, 8, 200)])
 @pytest.mark.parametrize("coll", ["bgk", "regularized"])
-def test_peer_ring_two_step_kernel(lb, nranks, ly, stride, nsteps, coll):
-    """Two-step kernel at N > 1 (peer mode): each launch first waits for both
-    neighbours' launch counters and copies their 6 edge columns into local
-    staging (k_tb_pull), then the two-step kernel reads columns beyond the slab
-    from there.  Steps in pairs (odd remainders: one-step peer launches, whose
-    halo pull follows a two-step launch) on separate streams == the 1-slab run
-    bit for bit."""
-    lx = 24
+@pytest.mark.parametrize("edge_pull", [True, False])
+def test_peer_ring_two_step_kernel(lb, nranks, ly, stride, nsteps, lx, coll, edge_pull):
+    """Two-step kernel at N > 1 (peer mode).  edge_pull (the default): only the
+    CTAs whose sweep comes within 6 columns of a slab edge wait for that
+    neighbour's launch counter and stage their strip's rows of its 6 edge
+    columns inside the kernel (interior CTAs start at once; with lx = 24 many
+    CTAs share an edge, with lx = 200 one per strip and side); else a k_tb_pull
+    launch stages whole columns first.  Steps in pairs (odd remainders:
+    one-step peer launches, whose halo pull follows a two-step launch) on
+    separate streams == the 1-slab run (one-step kernel) bit for bit."""
     lx_total = lx * nranks
     T0 = oracle.t0()
-    ref = lb.Lattice(lx_total, ly, collision=coll, gravity=(1e-6, -1e-5))
+    ref = lb.Lattice(lx_total, ly, collision=coll, gravity=(1e-6, -1e-5), temporal=False)   # one-step kernel
     ref.init_macro(*lbgen.rt_macro(lx_total, ly, T0))
     ref.step(nsteps)
     want = ref.gather()
@@ -419,6 +454,8 @@ def test_peer_ring_two_step_kernel(lb, nranks, ly, stride, nsteps, coll):
         g = lb.Lattice(lx_total, ly, rank=r, nranks=nranks, stream=torch.cuda.Stream(), collision=coll,
                        gravity=(1e-6, -1e-5))
         g.init_macro(*lbgen.rt_macro(lx_total, ly, T0, x0=r * lx, lx=lx))
+        g.edge_pull(edge_pull)
+        g.profile(True)
         ranks.append(g)
     for r, g in enumerate(ranks):
         g.set_peers(ranks[(r - 1) % nranks], ranks[(r + 1) % nranks])
@@ -433,6 +470,41 @@ def test_peer_ring_two_step_kernel(lb, nranks, ly, stride, nsteps, coll):
         g.sync()
     got = np.concatenate([g.peek(0) for g in ranks], axis=1)
     assert np.array_equal(got, want)
+    for g in ranks:
+        names = g.profile_read()
+        assert names.get("k_step2_tb" + ("_reg" if coll == "regularized" else ""), {}).get("launches", 0) > 0
+        assert ("k_tb_pull" in names) == (not edge_pull), names
+        g.close()
+
+
+@pytest.mark.parametrize("edge_pull", [True, False])
+def test_peer_ring_two_step_injected_delay(lb, edge_pull):
+    """Two-step kernel at N = 4 with an injected ~1 ms delay in front of one
+    rank's every launch: the edge CTAs' counter waits order the exchange, the
+    result is the 1-slab run bit for bit."""
+    lx, ly, n, nsteps = 60, 230, 4, 8
+    T0 = oracle.t0()
+    ref = lb.Lattice(lx * n, ly, temporal=False)
+    ref.init_macro(*lbgen.rt_macro(lx * n, ly, T0))
+    ref.step(nsteps)
+    streams = [torch.cuda.Stream() for _ in range(n)]
+    ranks = [lb.Lattice(lx * n, ly, rank=r, nranks=n, stream=streams[r]) for r in range(n)]
+    for r, g in enumerate(ranks):
+        g.init_macro(*lbgen.rt_macro(lx * n, ly, T0, x0=r * lx, lx=lx))
+        g.edge_pull(edge_pull)
+    for r, g in enumerate(ranks):
+        g.set_peers(ranks[(r - 1) % n], ranks[(r + 1) % n])
+    torch.cuda.synchronize()
+    for _ in range(nsteps // 2):
+        for r, g in enumerate(ranks):
+            if r == 1:
+                with torch.cuda.stream(streams[r]):
+                    torch.cuda._sleep(2_000_000)
+            g.step(2)
+    for g in ranks:
+        g.sync()
+    got = np.concatenate([g.peek(0) for g in ranks], axis=1)
+    assert np.array_equal(got, ref.gather())
     for g in ranks:
         g.close()
 
@@ -630,28 +702,52 @@ def test_tma_fused_step_bit_identical(lb, coll, bc, shape):
 
 # ------------------------------------------------------------------ two steps per pass (temporal blocking)
 
+TB_HT = 104   # strip height of the shipped two-step kernel (lb_tb.cu LB_TB_HT)
+
+
 @pytest.mark.parametrize("coll", ["bgk", "regularized"])
 @pytest.mark.parametrize("bc", ["thermal", "adiabatic"])
-@pytest.mark.parametrize("shape", [(6, 6), (24, 40), (17, 131), (64, 32), (9, 300), (131, 200), (12, 60), (10, 75),
-                                   (8, 146), (7, 147), (11, 72), (9, 76), (13, 145), (9, 211)])
+@pytest.mark.parametrize("shape", [(6, 6), (24, 40), (17, 131), (64, 32), (9, 300), (131, 200), (12, 60),
+                                   # the strip-layout edges of HT = 104 (strip_ya / tb_layout_ok):
+                                   (10, 104), (9, 105), (8, 107), (7, 109), (11, 110), (9, 111),
+                                   (9, 208), (13, 214), (9, 215), (8, 312), (7, 318)])
 def test_two_step_kernel_bit_identical(lb, coll, bc, shape):
     """LB_OPT_TEMPORAL (k_step2_tb: states n+1 and n+2 in one pass, n+1 kept in
-    shared memory) == two fused steps bit for bit: strips shorter than, equal
-    to and ragged against the 64-row strip height, a moved top strip, sweeps
-    that wrap periodically in x and CTA ranges that cross strip boundaries;
-    odd step counts end with one fused step."""
+    shared memory) == two one-step fused launches bit for bit, and both == the
+    oracle (<= 1e-12).  Shapes around the shipped strip height HT = 104:
+    exactly one strip (104), the band 105..109 where no strip layout keeps the
+    wall bands inside wall strips (lb_step must fall back to the one-step
+    kernel — asserted from the launch names), the moved second strip (110,
+    111), two exact strips (208) plus 6 / 7 rows (214, 215), three strips
+    (312, 318); sweeps that wrap periodically in x, CTA ranges that cross strip
+    boundaries; odd step counts end with one fused step."""
     lx, ly = shape
     st = oracle_state(lx, ly, seed=lx * 7 + ly)
+    grav = (1e-6, -1e-5)
     outs = []
     for tb in (False, True):
-        g = lb.Lattice(lx, ly, bc_y=bc, collision=coll, gravity=(1e-6, -1e-5))
-        if tb:
-            g.temporal(True)
+        g = lb.Lattice(lx, ly, bc_y=bc, collision=coll, gravity=grav, temporal=tb)
+        g.profile(True)
         g.set_state(st)
         g.step(4)
         g.step(3)
+        names = g.profile_read()
         outs.append(g.gather())
+        two = sum(v["launches"] for k, v in names.items() if k.startswith("k_step2_tb"))
+        if not tb:
+            assert two == 0, names
+        elif TB_HT < ly < TB_HT + 6:
+            assert two == 0 and names["k_step_fused_reg" if coll == "regularized" else "k_step_fused"][
+                "launches"] == 7, names
+        else:
+            assert two == 3, names   # 4 = 2 + 2, 3 = 2 + one fused step
+        g.close()
     assert np.array_equal(outs[0], outs[1])
+    o = oracle.Lattice(lx, ly, bc_y=BCN[bc], collision=oracle.REGULARIZED if coll == "regularized" else oracle.BGK,
+                       gravity=grav)
+    o.set_state(st)
+    o.step(7)
+    assert max_rel(outs[1], o.get_state(0)) < TOL
 
 
 def test_two_step_kernel_l2_promotion(lb):
@@ -660,7 +756,7 @@ def test_two_step_kernel_l2_promotion(lb):
     the tensor maps); other values are rejected."""
     lx, ly = 24, 230
     st = oracle_state(lx, ly, seed=11)
-    ref = lb.Lattice(lx, ly)
+    ref = lb.Lattice(lx, ly, temporal=False)   # one-step kernel reference
     ref.set_state(st)
     ref.step(4)
     for promo in (0, 64, 128, 256):
@@ -684,7 +780,7 @@ def test_two_step_kernel_grid_and_prefetch(lb, grid, l2, coll):
     kernel this also runs its mbarrier hand-over across many sweeps per CTA."""
     lx, ly = 40, 150
     st = oracle_state(lx, ly, seed=5)
-    ref = lb.Lattice(lx, ly, collision=coll)
+    ref = lb.Lattice(lx, ly, collision=coll, temporal=False)   # one-step kernel reference
     ref.set_state(st)
     ref.step(6)
     g = lb.Lattice(lx, ly, collision=coll)
@@ -832,3 +928,79 @@ def test_peer_ring_survey_geometries_with_injected_delay(lb, lx_total, ly, n):
     assert np.array_equal(got, ref.gather())
     for g in ranks:
         g.close()
+
+
+# ------------------------------------------------------------------ failure detection
+
+def _inject_nan(g, x, y, l=11):
+    """A blow-up mid-run: NaN written straight into BOTH device buffers at one
+    physical site (whichever holds the current state), bypassing the API."""
+    L = g.layout
+    idx = ((3 + x) * 37 + l) * L.nyp + L.y0 + y
+    for b in g.bufs:
+        b[idx] = float("nan")
+    torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("temporal", [False, True])
+def test_nan_mid_run_raises_enonphys_at_sync(lb, temporal):
+    """SPEC S:298 / S:469: a NaN appearing mid-run on the monitored asynchronous
+    path (one-step kernel + lb_invariants_async, or the two-step kernel +
+    lb_invariants_pair_async) sets the device non-physical flag, and the next
+    lb_sync returns LB_ENONPHYS; the flag is sticky until the state is
+    replaced, and a clean state clears it."""
+    lx, ly = 48, 150
+    g = lb.Lattice(lx, ly, temporal=temporal, stream=torch.cuda.Stream())
+    fields = lbgen.rt_macro(lx, ly, oracle.t0())
+    g.init_macro(*fields)
+    g.monitor(True)
+    out = torch.zeros(10, dtype=torch.float64).pin_memory()
+    for _ in range(2):                                  # healthy steps: no error
+        g.step(2)
+        (g.invariants_pair_async if temporal else g.invariants_async)(out)
+        g.sync()
+    assert out[4] > 0.5
+    _inject_nan(g, 17, 60)
+    g.step(2)
+    (g.invariants_pair_async if temporal else g.invariants_async)(out)
+    with pytest.raises(lb.LBError) as ei:
+        g.sync()
+    assert ei.value.status == 5
+    if temporal:   # caught in the first state of the pair: the step where it spread
+        assert out[4] == -np.inf
+    with pytest.raises(lb.LBError) as ei:               # sticky
+        g.sync()
+    assert ei.value.status == 5
+    g.init_macro(*fields)                               # a clean state clears it
+    g.step(2)
+    (g.invariants_pair_async if temporal else g.invariants_async)(out)
+    g.sync()
+    assert out[4] > 0.5
+    g.close()
+
+
+def test_nonphysical_flag_from_collision_output(lb):
+    """A blow-up created by a collision is flagged by the launch that performs
+    it: the state is finite everywhere, but after propagate one site holds
+    rho = 0 with momentum (its pulled populations: +0.25 along (1,0), -0.25
+    along (-1,0), all others 0) — the collision then produces non-finite
+    values (u = j/rho), and the two-step launch's own monitors set the flag."""
+    lx, ly = 40, 64
+    st = oracle_state(lx, ly, seed=8)
+    c = oracle.velocities()
+    x, y = 20, 30
+    for l in range(Q):            # the pull sources of site (x, y): x - c_l
+        st[l, x - c[l, 0], y - c[l, 1]] = 0.0
+    st[11, x - 1, y], st[25, x + 1, y] = 0.25, -0.25
+    assert tuple(c[11]) == (1, 0) and tuple(c[25]) == (-1, 0)
+    assert np.all(np.isfinite(st))
+    g = lb.Lattice(lx, ly, bc_y="adiabatic")
+    g.set_state(st)
+    g.monitor(True)
+    g.step(2)
+    out = np.zeros(10)
+    g.invariants_pair_async(out)
+    with pytest.raises(lb.LBError) as ei:
+        g.sync()
+    assert ei.value.status == 5
+    assert not out[4] > 0.0       # state n+1's minimum: the collision at (x, y)

@@ -360,9 +360,44 @@ def test_thermal_wall_sets_u0_and_twall():
             m = oracle.macro(out[:, x, y])
             assert abs(m[1]) < 1e-15 and abs(m[2]) < 1e-15
             assert abs(m[3] - (1.05 if y < 3 else 0.95) * T0) < 1e-14
-        for y in range(3, ly - 3):   # interior rows untouched by bc
-            assert np.array_equal(out[:, x, y], out[:, x, y])
     assert pre.shape == out.shape
+
+
+@pytest.mark.parametrize("bc", [oracle.WALL_THERMAL, oracle.WALL_ADIABATIC])
+@pytest.mark.parametrize("ly", [6, 7, 11])
+def test_bc_touches_only_the_three_rows_next_to_each_wall(bc, ly):
+    """Reading G9 / SURVEY §8c O6: bc rewrites exactly the rows [0, 3) and
+    [ly-3, ly) — the rows whose pull sources can lie beyond a wall (|c_y| <= 3).
+    Every row in [3, ly-3) after propagate + bc equals, bit for bit, a
+    brute-force periodic-x pull from the pre-step state written here with numpy
+    indexing (independent of the oracle's propagate): a band that is too wide
+    (or a bc writing interior rows) fails this; so does a band that is too
+    narrow (the third row keeps raw y-halo zeros, caught below)."""
+    lx = 9
+    c = oracle.velocities()
+    L = oracle.Lattice(lx, ly, bc_y=bc)
+    st = lbgen.random_field(Q, lx, ly, seed=100 + ly)
+    L.set_state(st)
+    L.pbc()
+    L.propagate()
+    L.bc()
+    out = L.get_state(1)
+    for l in range(Q):
+        cx, cy = int(c[l, 0]), int(c[l, 1])
+        for y in range(3, ly - 3):
+            assert 0 <= y - cy < ly
+            want = st[l, (np.arange(lx) - cx) % lx, y - cy]
+            assert np.array_equal(out[l, :, y], want), (l, y)
+    # the band rows are all rewritten: no entry pulled from the zero y-halo survives
+    for y in list(range(3)) + list(range(ly - 3, ly)):
+        assert np.all(out[:, :, y] != 0.0), y
+    if bc == oracle.WALL_THERMAL:
+        # (ii) repopulates every band site (rho K_wall), so row 2 (the third
+        # row) differs from its raw pull for at least one population
+        for y in (2, ly - 3):
+            raw = np.stack([st[l, (np.arange(lx) - c[l, 0]) % lx, min(max(y - c[l, 1], 0), ly - 1)]
+                            for l in range(Q)])
+            assert not np.array_equal(out[:, :, y], raw), y
 
 
 def test_uniform_wall_equilibrium_is_fixed_point():
@@ -391,6 +426,50 @@ def test_periodic_step_conserves_invariants():
     inv = L.invariants(0)
     assert np.all(np.isfinite(inv))
     assert np.abs(inv - inv0).max() / inv0[0] < 1e-13
+
+
+@pytest.mark.parametrize("which", [0, 1])
+def test_invariants_single_population_closed_form(which):
+    """lbref_invariants (the checker behind every GPU monitor test), pinned to
+    the definitions rho = sum f, j = sum c f, E = 1/2 sum |c|^2 f (Eq. 2,
+    P:189-197; SURVEY §8b lb_invariants): a lattice holding one population of
+    value v at label l (all else zero) must give exactly (v, v c_lx, v c_ly,
+    v |c_l|^2 / 2) — a swapped j_x / j_y, a dropped 1/2 or a wrong |c|^2 fails.
+    The labels' velocities are the paper-pinned table (P:452-453 and the
+    shell-count test above); v and its products are exact in binary."""
+    lx, ly = 5, 7
+    c = oracle.velocities()
+    for l in range(Q):
+        L = oracle.Lattice(lx, ly, bc_y=oracle.PERIODIC)
+        st = np.zeros((Q, lx, ly))
+        v = 0.375 + l / 64.0
+        st[l, l % lx, (3 * l) % ly] = v
+        L.set_state(st)
+        if which == 1:
+            L.pbc()
+            L.propagate()   # a permutation: the single value moves, the sums do not change
+        inv = L.invariants(which)
+        cx, cy = int(c[l, 0]), int(c[l, 1])
+        assert inv[0] == v and inv[1] == v * cx and inv[2] == v * cy, l
+        assert inv[3] == 0.5 * v * (cx * cx + cy * cy), l
+
+
+def test_invariants_are_additive_over_sites():
+    """Sum of the single-site closed forms over a whole random lattice: the
+    invariants of the field equal, to rounding, the sum over sites of each
+    site's (rho, j, E) computed here from the per-site moments of oracle.macro
+    (pinned separately to Eq. 2) — rho u = j, and E = rho (|u|^2 + D T) / 2."""
+    lx, ly = 6, 8
+    st = lbgen.random_field(Q, lx, ly, seed=23)
+    L = oracle.Lattice(lx, ly, bc_y=oracle.PERIODIC)
+    L.set_state(st)
+    inv = L.invariants(0)
+    acc = np.zeros(4)
+    for x in range(lx):
+        for y in range(ly):
+            rho, ux, uy, T = oracle.macro(st[:, x, y])
+            acc += [rho, rho * ux, rho * uy, 0.5 * rho * (ux * ux + uy * uy + 2.0 * T)]
+    assert np.allclose(inv, acc, rtol=1e-13, atol=1e-14 * acc[0])
 
 
 def test_walled_rt_step_conserves_mass_and_stays_physical():

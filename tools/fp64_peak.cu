@@ -1,6 +1,7 @@
 // FP64 DFMA peak and HBM copy microbenchmark (SURVEY.md §8d "FP64 peak microbenchmark").
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o fp64_peak fp64_peak.cu
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 #define CK(x) do{cudaError_t e=(x); if(e!=cudaSuccess){printf("CUDA %s @%d\n",cudaGetErrorString(e),__LINE__); return 1;}}while(0)
 
@@ -25,7 +26,8 @@ __global__ void copy_v2(const double2* __restrict__ a, double2* __restrict__ b, 
   for (; i < n; i += st) b[i] = a[i];
 }
 
-int main() {
+int main(int argc, char** argv) {
+  const int reps = argc > 1 ? atoi(argv[1]) : 5;   // timed DFMA launches (best one reported)
   int sms; CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
   int clk; CK(cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0));
   int l2; CK(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, 0));
@@ -35,7 +37,7 @@ int main() {
   dfma_chains<CH><<<blocks, TPB>>>(out, 1000, 1.0000001);
   CK(cudaDeviceSynchronize());
   float best = 1e30f;
-  for (int r = 0; r < 5; ++r) {
+  for (int r = 0; r < reps; ++r) {
     cudaEventRecord(e0); dfma_chains<CH><<<blocks, TPB>>>(out, iters, 1.0000001); cudaEventRecord(e1);
     CK(cudaEventSynchronize(e1)); float ms; cudaEventElapsedTime(&ms, e0, e1); if (ms < best) best = ms;
   }
