@@ -876,7 +876,7 @@ static int step_tb(lb_ctx* c) {
     pull.my_done = reinterpret_cast<const unsigned long long*>(P.my_done);
     pull.status = c->d_status;
     pull.timeout_ns = c->peer_timeout_ns;
-  } else if (peers)  // LB_OPT_TB_EDGE_PULL = 0: wait for both neighbours, copy their 6 edge columns, then the kernel
+  } else if (peers) {  // LB_OPT_TB_EDGE_PULL = 0: wait for both neighbours, copy their 6 edge columns, then the kernel
     TRY(launch(c, "k_tb_pull", c->s, 12LL * c->g.ly, [&] {
       return lbk::launch_tb_pull(c->g, c->d_stage, P.left_buf[c->par], P.right_buf[c->par],
                                  reinterpret_cast<const unsigned long long*>(P.left_done),
@@ -884,6 +884,8 @@ static int step_tb(lb_ctx* c) {
                                  reinterpret_cast<const unsigned long long*>(P.my_done), c->d_status,
                                  c->peer_timeout_ns, c->s);
     }));
+    c->launches += 1;  // two kernels: k_tb_wait (one block) + the k_tb_pull copy
+  }
   TRY(launch(c, c->p.collision ? "k_step2_tb_reg" : "k_step2_tb", c->s, 2 * c->L.sites, [&] {
     return lbk::launch_step2_tb(c->g, c->tb, c->par, c->B, c->p.bc_y, c->p.collision, c->relax, grid, c->tb_l2,
                                 c->tb_wall_w16, mon, peers ? 1 : 0, inpull ? &pull : nullptr, c->s);

@@ -56,8 +56,17 @@
 #include "lb_device.cuh"
 #include "lb_internal.h"
 
+#ifndef LB_TB_LEAD  // lead-in weight of a sweep in the work split (0: none)
+#define LB_TB_LEAD 7
+#endif
 #ifndef LB_TB_STCS
 #define LB_TB_STCS 0
+#endif
+#ifndef LB_TB_CLOCK  // variant builds only: per-CTA start/end times (tools/tb_clock.py)
+#define LB_TB_CLOCK 0
+#endif
+#if LB_TB_CLOCK
+__device__ unsigned long long g_tb_clock[1024 * 4];
 #endif
 
 namespace lbk {
@@ -146,7 +155,8 @@ struct TbCfg {
   static constexpr int S0_DBL = NB * BUFD;
   static constexpr int S1_DBL = SLOTS1_BEFORE(Q) * R1;
   // mbarriers: NB TMA buffers + (LB_TB_DECOUPLE) 2 full + 2 empty ring barriers
-  static constexpr size_t SMEM = (size_t)(S0_DBL + S1_DBL) * sizeof(double) + (NB + 4) * sizeof(uint64_t);
+  // + (LB_TB_ISSUE2) NB "phase 1 gathered buffer b" barriers
+  static constexpr size_t SMEM = (size_t)(S0_DBL + S1_DBL) * sizeof(double) + (2 * NB + 4) * sizeof(uint64_t);
   static_assert(RB % 2 == 0 && RB <= 256, "TMA box rows");
   static_assert(SMEM <= 232448, "shared memory per CTA");
   static_assert(NW <= 8, "two warps per scheduler at most (64 KB register file per scheduler)");
@@ -424,6 +434,14 @@ __device__ __forceinline__ void phase2(const double* s1, double* __restrict__ B,
 #ifndef LB_TB_NBAR
 #define LB_TB_NBAR 0
 #endif
+// ISSUE2: the phase-2 warps (which wait at the iteration barrier for phase 1)
+// refill the state-n buffers: each phase-1 thread arrives on gath[b] right
+// after its gather from buffer b, and the issuing phase-2 lanes wait for that
+// arrival and load iteration t + NB's windows into b — instead of the phase-1
+// warps meeting at a named barrier after the gather and issuing themselves.
+#ifndef LB_TB_ISSUE2
+#define LB_TB_ISSUE2 0
+#endif
 constexpr int TB_HT = LB_TB_HT;
 constexpr int TB_PF = LB_TB_PF;
 using Cfg = TbCfg<TB_HT, TB_PF>;
@@ -522,6 +540,7 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
   // Arrivals (t = 0 .. niter - 2) and syncs (t = 1 .. niter - 1) pair up
   // within a sweep, so no generation is left open across sweeps.
   constexpr bool NBAR = !DECOUPLE && ((LB_TB_NBAR >> (COLL == COLL_REGULARIZED ? 1 : 0)) & 1);
+  constexpr bool ISSUE2 = EARLY && !NBAR && ((LB_TB_ISSUE2 >> (COLL == COLL_REGULARIZED ? 1 : 0)) & 1);
   static_assert(!NBAR || EARLY, "named-barrier hand-over needs the phase-1 warps to issue the loads");
   extern __shared__ __align__(128) double sm[];
   double* s0 = sm;
@@ -537,6 +556,8 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bars + NB + i)), "r"(32 * C::NW1));
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bars + NB + 2 + i)), "r"(32 * C::NW2));
     }
+    for (int i = 0; i < NB; ++i)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bars + NB + 4 + i)), "r"(32 * C::NW1));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -545,11 +566,21 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
   // one (thermal repopulation and mirror copies on its wall warps), so the CTAs
   // that sweep wall strips get proportionally fewer columns.  unit_at(T): the
   // first (strip, column) unit whose weighted start is >= T.
+  // A sweep costs its W columns plus a lead-in of TB_LEAD iterations (phase 1
+  // starts 6 columns early, phase 2 lags 1 more), and a range that crosses a
+  // strip start pays a second lead-in: so every strip but the first is
+  // preceded by TB_LEAD columns of weight, which the range holding that strip
+  // start absorbs (unit_at maps T inside it to the strip start).
+  constexpr int TB_LEAD = LB_TB_LEAD;
   auto strip_w = [&](int s) { return (nstrips > 1 && (s == 0 || s == nstrips - 1)) ? wall_w16 : 16; };
   auto unit_at = [&](int64_t T) -> int64_t {
     int64_t acc = 0;
     for (int s = 0; s < nstrips; ++s) {
       const int w = strip_w(s);
+      if (s > 0) {
+        acc += (int64_t)TB_LEAD * w;
+        if (T < acc) return (int64_t)s * lx;
+      }
       const int64_t sw = (int64_t)lx * w;
       if (T < acc + sw) return (int64_t)s * lx + (T - acc + w - 1) / w;
       acc += sw;
@@ -557,9 +588,14 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
     return (int64_t)nstrips * lx;
   };
   int64_t wtot = 0;
-  for (int s = 0; s < nstrips; ++s) wtot += (int64_t)lx * strip_w(s);
+  for (int s = 0; s < nstrips; ++s) wtot += (int64_t)(lx + (s > 0 ? TB_LEAD : 0)) * strip_w(s);
   int64_t u = unit_at(wtot * blockIdx.x / gridDim.x);
   const int64_t u_end = unit_at(wtot * (blockIdx.x + 1) / gridDim.x);
+#if LB_TB_CLOCK
+  unsigned long long clk0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(clk0));
+  int nsweeps = 0;
+#endif
   uint32_t kglob = 0;  // load iterations of this CTA over all its sweeps (barrier phase)
   uint32_t iglob = 0;  // DECOUPLE: iterations of this CTA over all its sweeps (ring items)
   const uint32_t bar_full = smem_u32(bars + NB), bar_empty = smem_u32(bars + NB + 2);
@@ -571,6 +607,9 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
     const int x1 = (int)std::min<int64_t>(lx, x0 + (u_end - u));
     u += x1 - x0;
     const int xs = H + x0, W = x1 - x0;  // output columns [xs, xs + W)
+#if LB_TB_CLOCK
+    nsweeps += 1;
+#endif
     // strip rows [ya, ya + HT) (strip_ya); the top strip may reach one row
     // past the wall, which is simply not computed
     const int ya = strip_ya(strip, nstrips, ly, HT);
@@ -635,11 +674,14 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
           : "memory");
     };
     // lanes [0, GPW) of warp w issue groups GPW w + lane (EARLY: the phase-1
-    // warps only — they refill their single buffer right after gathering from it)
-    constexpr int NWI = EARLY ? C::NW1 : (C::NW < NG ? C::NW : NG);
+    // warps only — they refill their single buffer right after gathering from
+    // it; ISSUE2: the phase-2 warps)
+    constexpr int NWI = ISSUE2 ? C::NW2 : EARLY ? C::NW1 : (C::NW < NG ? C::NW : NG);
     constexpr int GPW = (NG + NWI - 1) / NWI;
-    const int my_grp = GPW * warp + (tid & 31);
-    const bool issuer = warp < NWI && (tid & 31) < GPW && my_grp < NG;
+    const int wi = ISSUE2 ? warp - C::NW1 : warp;
+    const int my_grp = GPW * wi + (tid & 31);
+    const bool issuer = wi >= 0 && wi < NWI && (tid & 31) < GPW && my_grp < NG;
+    const uint32_t bar_gath = smem_u32(bars + NB + 4);
 
     if (issuer)
       for (int k = 0; k < (EARLY ? NB : PF) && k < nload; ++k) issue_one(k, my_grp);
@@ -695,8 +737,12 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
             // with iteration t + NB's windows while the collisions run
             double f[Q];
             phase1_gather<BUFD, RB>(s0, buf, valid ? i : 0, f);
-            asm volatile("bar.sync 2, %0;" ::"r"(32 * C::NW1) : "memory");
-            if (issuer && t + NB < nload) issue_one(t + NB, my_grp);
+            if (ISSUE2) {  // buffer buf read: the phase-2 issuers may refill it
+              asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar_gath + 8 * buf) : "memory");
+            } else {
+              asm volatile("bar.sync 2, %0;" ::"r"(32 * C::NW1) : "memory");
+              if (issuer && t + NB < nload) issue_one(t + NB, my_grp);
+            }
             if (NBAR) {
               if (valid) phase1_collide<COLL, MON>(f, y, ly, thermal, r, own, acc);
               if (t > 0) asm volatile("bar.sync %0, %1;" ::"r"(5 + ((t - 1) & 1)), "r"(C::NT) : "memory");
@@ -733,6 +779,27 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
         double f[Q];
         if (t >= 7) phase2_gather<R1>(s1, t, valid ? i : 0, f);
         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar_empty + 8 * (I & 1)) : "memory");
+        if (ISSUE2 && issuer && t + NB < nload) {  // see the ISSUE2 branch below
+          const uint32_t kb = kglob + (uint32_t)t;
+          mbar_wait(bar_gath + 8 * (kb % NB), (kb / NB) & 1);
+          issue_one(t + NB, my_grp);
+        }
+        if (valid)
+          phase2_update<COLL, MON>(f, B, g, y, xs - 7 + t, thermal, r, y >= own_lo && y < own_hi, acc, !peers);
+      } else if (ISSUE2) {
+        // phase 2: state n+2 at column c2 = xs - 7 + t, rows [ya, ya+HT);
+        // after its gather, the issuing lanes wait until phase 1 gathered from
+        // this iteration's state-n buffer and refill it with iteration t + NB's
+        const int i = tid - 32 * C::NW1;
+        const int y = ya + i;
+        const bool valid = t >= 7 && i < HT && y < ly;
+        double f[Q];
+        if (t >= 7) phase2_gather<R1>(s1, t, valid ? i : 0, f);
+        if (issuer && t + NB < nload) {
+          const uint32_t kb = kglob + (uint32_t)t;
+          mbar_wait(bar_gath + 8 * (kb % NB), (kb / NB) & 1);
+          issue_one(t + NB, my_grp);
+        }
         if (valid)
           phase2_update<COLL, MON>(f, B, g, y, xs - 7 + t, thermal, r, y >= own_lo && y < own_hi, acc, !peers);
       } else if (t >= 7) {
@@ -754,6 +821,18 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
     iglob += (uint32_t)niter;
     __syncthreads();  // the next sweep refills every ring
   }
+#if LB_TB_CLOCK
+  if (tid == 0 && blockIdx.x < 1024) {
+    unsigned long long clk1;
+    unsigned int smid;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(clk1));
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_tb_clock[4 * blockIdx.x + 0] = clk0;
+    g_tb_clock[4 * blockIdx.x + 1] = clk1;
+    g_tb_clock[4 * blockIdx.x + 2] = smid;
+    g_tb_clock[4 * blockIdx.x + 3] = ((unsigned long long)nsweeps << 32) | (unsigned)iglob;
+  }
+#endif
   if (MON) {
     // warp xor-tree, then the warps of each phase in order (deterministic)
 #pragma unroll
@@ -907,16 +986,20 @@ cudaError_t launch_step2_tb(const Geo& g, const TbMaps* t, int src_buf, double* 
 // ---- N > 1: staging of the neighbours' edge columns (peer memory -> local)
 namespace {
 
-// Every block's thread 0 waits until both neighbours completed as many launches
-// as this rank (their current buffer then holds the same state as ours, and
-// they are done reading our previous one), then the grid copies the left
-// neighbour's internal columns [lx-3, lx+3) and the right one's [3, 9).
-__global__ void __launch_bounds__(256) k_tb_pull(double2* __restrict__ stage, const double2* L, const double2* R,
-                                                 int64_t lx, int64_t cs2, const unsigned long long* waitL,
-                                                 const unsigned long long* waitR, const unsigned long long* my_done,
-                                                 unsigned int* status, unsigned long long timeout_ns) {
+// One thread waits until both neighbours completed as many launches as this
+// rank (their current buffer then holds the same state as ours, and they are
+// done reading our previous one); the copy kernel behind it on the stream then
+// stages the left neighbour's internal columns [lx-3, lx+3) and the right
+// one's [3, 9).  The wait is a one-block kernel of its own so that a waiting
+// rank holds one SM slot, not a grid of spinning blocks (ranks sharing one GPU
+// in tests would otherwise starve the neighbour they wait for).
+__global__ void k_tb_wait(const unsigned long long* waitL, const unsigned long long* waitR,
+                          const unsigned long long* my_done, unsigned int* status, unsigned long long timeout_ns) {
   if (threadIdx.x == 0) peer_wait(waitL, waitR, my_done, status, timeout_ns);
-  __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) k_tb_pull(double2* __restrict__ stage, const double2* L, const double2* R,
+                                                 int64_t lx, int64_t cs2) {
   const int64_t n = 6 * cs2;  // double2 per side
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 2 * n; i += (int64_t)gridDim.x * blockDim.x)
     stage[i] = i < n ? __ldcg(L + (lx - 3) * cs2 + i) : __ldcg(R + 3 * cs2 + (i - n));
@@ -942,10 +1025,16 @@ cudaError_t launch_tb_pull(const Geo& g, double* stage, const double* left_A, co
                            cudaStream_t s) {
   const int64_t cs2 = g.cs / 2;
   const int blocks = (int)std::min<int64_t>((12 * cs2 + 255) / 256, 148 * 4);
+  k_tb_wait<<<1, 32, 0, s>>>(waitL, waitR, my_done, status, timeout_ns);
   k_tb_pull<<<blocks, 256, 0, s>>>(reinterpret_cast<double2*>(stage), reinterpret_cast<const double2*>(left_A),
-                                   reinterpret_cast<const double2*>(right_A), g.lx, cs2, waitL, waitR, my_done,
-                                   status, timeout_ns);
+                                   reinterpret_cast<const double2*>(right_A), g.lx, cs2);
   return cudaGetLastError();
 }
 
 }  // namespace lbk
+
+#if LB_TB_CLOCK
+extern "C" int lb_debug_tb_clock(unsigned long long* host, int n) {
+  return (int)cudaMemcpyFromSymbol(host, g_tb_clock, sizeof(unsigned long long) * 4 * (n < 1024 ? n : 1024));
+}
+#endif

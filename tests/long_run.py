@@ -66,8 +66,14 @@ class Ring:
         torch.cuda.synchronize()
 
     def step(self, k):
-        for g in self.slabs:
-            g.step(k)
+        # interleave the slabs per launch (2 steps, or an odd remainder of 1):
+        # on the one shared stream, slab r's launch j+1 waits for its
+        # neighbours' launch j, which must already be queued ahead of it
+        while k > 0:
+            s = 2 if k >= 2 else 1
+            for g in self.slabs:
+                g.step(s)
+            k -= s
 
     def sync(self):
         for g in self.slabs:
