@@ -342,7 +342,8 @@ int lb_sync(lb_ctx* ctx);
  * fused steps; an odd remainder takes one fused step.  LB_OPT_TB_GRID: CTAs of
  * that kernel (0 = one per SM), LB_OPT_TB_L2_PREFETCH: L2 prefetch distance in
  * columns (0 = off, the default, <= 64; per-line prefetch of the newest column).  LB_OPT_TB_WALL_WEIGHT: cost of a column of a
- * wall strip relative to an interior one, x16 (work split; default 20).
+ * wall strip relative to an interior one, x16 (work split; 0 = the default: 19 for BGK, 20 for the
+ * regularised collide).
  * LB_OPT_TB_L2_PROMOTION: L2 promotion of that kernel's TMA window loads in
  * bytes (0 = none, 64 = default, 128, 256); results do not depend on it.
  * LB_OPT_TB_EDGE_PULL (N > 1, peer mode): 1 (default) = the exchange runs
@@ -389,6 +390,12 @@ int lb_profile_reset(lb_ctx* ctx);
 int lb_profile_read(lb_ctx* ctx, lb_kprof* out, int max, int* n);
 /* Number of kernel launches the library issued since lb_init (all streams). */
 int64_t lb_launch_count(const lb_ctx* ctx);
+/* Strip height HT of the two-step kernel this library was built with (rows a
+ * CTA computes per sweep).  lb_step uses that kernel for
+ * ly <= HT or ly >= HT + 6 (other heights admit no strip layout that keeps
+ * each wall band inside a wall strip) and the one-step kernel otherwise.
+ * No context, no GPU needed. */
+int lb_tb_strip_height(void);
 
 #ifdef __cplusplus
 }

@@ -149,7 +149,7 @@ struct lb_ctx {
   int tb_grid = 0;              // LB_OPT_TB_GRID: CTAs of the two-step kernel (0 = SM count)
   int tb_l2 = 0;                // LB_OPT_TB_L2_PREFETCH: L2 prefetch distance in columns
   int tb_promo = 64;            // LB_OPT_TB_L2_PROMOTION: L2 promotion of its TMA loads (bytes)
-  int tb_wall_w16 = 20;         // LB_OPT_TB_WALL_WEIGHT: wall-strip column cost x16 (work split)
+  int tb_wall_w16 = 0;          // LB_OPT_TB_WALL_WEIGHT: wall-strip column cost x16 (work split; 0 = per collision)
   int tb_edge_pull = 1;         // LB_OPT_TB_EDGE_PULL: N > 1 two-step exchange inside the kernel (1) or k_tb_pull first (0)
   double* d_stage = nullptr;    // N > 1 two-step: the neighbours' 6 edge columns (2 x 6 x cs doubles)
   double* d_mon_tb = nullptr;   // two-step monitors: 2 x cap x 5 per-CTA partials, then reduce scratch
@@ -851,6 +851,15 @@ static bool tb_usable(const lb_ctx* c) {
          lbk::tb_layout_ok(c->g.ly);
 }
 
+// Cost of a wall-strip column relative to an interior one (x16) in the
+// two-step kernel's work split: measured per-CTA times (tools/tb_clock.py,
+// 1920x2048) give 1.17 (BGK) and 1.25 (regularised) per iteration, and a
+// sweep of the BGK weight 17..21 peaks at 19.
+static int tb_wall_weight(const lb_ctx* c) {
+  if (c->tb_wall_w16 > 0) return c->tb_wall_w16;
+  return c->p.collision == LB_COLLIDE_REGULARIZED ? 20 : 19;
+}
+
 static int step_tb(lb_ctx* c) {
   const int grid = c->tb_grid > 0 ? c->tb_grid : c->sm_count;
   const int G = lbk::tb_grid(c->g, grid);
@@ -888,7 +897,7 @@ static int step_tb(lb_ctx* c) {
   }
   TRY(launch(c, c->p.collision ? "k_step2_tb_reg" : "k_step2_tb", c->s, 2 * c->L.sites, [&] {
     return lbk::launch_step2_tb(c->g, c->tb, c->par, c->B, c->p.bc_y, c->p.collision, c->relax, grid, c->tb_l2,
-                                c->tb_wall_w16, mon, peers ? 1 : 0, inpull ? &pull : nullptr, c->s);
+                                tb_wall_weight(c), mon, peers ? 1 : 0, inpull ? &pull : nullptr, c->s);
   }));
   if (peers) {  // publish: this launch is complete (the neighbours may now read our new state)
     c->peer_step += 1;
@@ -1165,7 +1174,7 @@ int lb_set_option(lb_ctx* c, int option, int value) {
       if (c->tb && !lbk::tb_set_promotion(c->tb, c->g, value)) return fail(LB_ECUDA, "tensor-map re-encoding failed");
       return LB_OK;
     case LB_OPT_TB_WALL_WEIGHT:
-      if (value < 1 || value > 256) return fail(LB_EINVAL, "wall weight (x16) must be in [1, 256]");
+      if (value < 0 || value > 256) return fail(LB_EINVAL, "wall weight (x16) must be in [0 (auto), 256]");
       c->tb_wall_w16 = value;
       return LB_OK;
     case LB_OPT_TB_EDGE_PULL:
@@ -1227,5 +1236,7 @@ int lb_profile_read(lb_ctx* c, lb_kprof* out, int max, int* n) {
 }
 
 int64_t lb_launch_count(const lb_ctx* c) { return c ? c->launches : -1; }
+
+int lb_tb_strip_height(void) { return lbk::tb_strip_height(); }
 
 }  // extern "C"

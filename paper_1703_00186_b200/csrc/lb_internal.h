@@ -109,6 +109,7 @@ cudaError_t launch_tb_pull(const Geo& g, double* stage, const double* left_A, co
                            cudaStream_t s);
 // false for the few heights with no valid strip layout (HT < ly < HT + 6)
 bool tb_layout_ok(int ly);
+int tb_strip_height();  // HT of the compiled two-step kernel
 void tb_destroy(TbMaps* t);
 // lb_tb.cu's own copies of the wall constants and the Gram inverse
 cudaError_t tb_upload_constants(const double* k_bottom, const double* k_top, const double* ginv, cudaStream_t s);

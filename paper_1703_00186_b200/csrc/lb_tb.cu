@@ -155,8 +155,7 @@ struct TbCfg {
   static constexpr int S0_DBL = NB * BUFD;
   static constexpr int S1_DBL = SLOTS1_BEFORE(Q) * R1;
   // mbarriers: NB TMA buffers + (LB_TB_DECOUPLE) 2 full + 2 empty ring barriers
-  // + (LB_TB_ISSUE2) NB "phase 1 gathered buffer b" barriers
-  static constexpr size_t SMEM = (size_t)(S0_DBL + S1_DBL) * sizeof(double) + (2 * NB + 4) * sizeof(uint64_t);
+  static constexpr size_t SMEM = (size_t)(S0_DBL + S1_DBL) * sizeof(double) + (NB + 4) * sizeof(uint64_t);
   static_assert(RB % 2 == 0 && RB <= 256, "TMA box rows");
   static_assert(SMEM <= 232448, "shared memory per CTA");
   static_assert(NW <= 8, "two warps per scheduler at most (64 KB register file per scheduler)");
@@ -294,6 +293,12 @@ __device__ __forceinline__ void acc_invariants(const Macro& m, const Relax& r, d
 #ifndef LB_TB_FAKE
 #define LB_TB_FAKE 0
 #endif
+// LB_TB_NOLOAD (variant builds only, timing experiments): no state-n loads and
+// no waits for them — the compute + stores of the kernel alone (results are
+// then meaningless)
+#ifndef LB_TB_NOLOAD
+#define LB_TB_NOLOAD 0
+#endif
 // The collision of both phases.  LB_TB_FAKE (variant builds only, timing
 // experiments): a one-multiply stand-in, to time the kernel's data-movement
 // skeleton without the FP64 work (results are then meaningless).
@@ -332,6 +337,11 @@ __device__ __forceinline__ void phase1_collide(double (&f)[Q], int y, int ly, bo
 }
 
 // state n+1 of row y into the ring slot of iteration t (+ the virtual rows it mirrors into)
+// (Measured and rejected: slots of HT rows instead of R1 = HT + 6 — phase 1
+// stores row i at i - 3 + cy_l when in range, phase 2 reads its own row — which
+// frees the shared memory for HT = 108 (19 strips instead of 20 at ly = 2048):
+// 16.30K MLUPS, and 16.33K at HT = 104, against 16.55K for this layout; the
+// per-population store predicates cost more than the 5 % fewer iterations save.)
 template <int R1>
 __device__ __forceinline__ void phase1_store(const double (&f)[Q], double* s1, int t, int i, int y, int ly) {
   const int io = opaque(i);
@@ -434,14 +444,6 @@ __device__ __forceinline__ void phase2(const double* s1, double* __restrict__ B,
 #ifndef LB_TB_NBAR
 #define LB_TB_NBAR 0
 #endif
-// ISSUE2: the phase-2 warps (which wait at the iteration barrier for phase 1)
-// refill the state-n buffers: each phase-1 thread arrives on gath[b] right
-// after its gather from buffer b, and the issuing phase-2 lanes wait for that
-// arrival and load iteration t + NB's windows into b — instead of the phase-1
-// warps meeting at a named barrier after the gather and issuing themselves.
-#ifndef LB_TB_ISSUE2
-#define LB_TB_ISSUE2 0
-#endif
 constexpr int TB_HT = LB_TB_HT;
 constexpr int TB_PF = LB_TB_PF;
 using Cfg = TbCfg<TB_HT, TB_PF>;
@@ -540,7 +542,6 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
   // Arrivals (t = 0 .. niter - 2) and syncs (t = 1 .. niter - 1) pair up
   // within a sweep, so no generation is left open across sweeps.
   constexpr bool NBAR = !DECOUPLE && ((LB_TB_NBAR >> (COLL == COLL_REGULARIZED ? 1 : 0)) & 1);
-  constexpr bool ISSUE2 = EARLY && !NBAR && ((LB_TB_ISSUE2 >> (COLL == COLL_REGULARIZED ? 1 : 0)) & 1);
   static_assert(!NBAR || EARLY, "named-barrier hand-over needs the phase-1 warps to issue the loads");
   extern __shared__ __align__(128) double sm[];
   double* s0 = sm;
@@ -556,8 +557,6 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bars + NB + i)), "r"(32 * C::NW1));
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bars + NB + 2 + i)), "r"(32 * C::NW2));
     }
-    for (int i = 0; i < NB; ++i)
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bars + NB + 4 + i)), "r"(32 * C::NW1));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -648,6 +647,7 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
     // group; the thread of g = 0 also posts the expected bytes (complete_tx may
     // precede it: the phase cannot complete before that single arrival)
     auto issue_one = [&](int k, int gq) {
+      if (LB_TB_NOLOAD) return;
       const uint32_t kb = kglob + (uint32_t)k;
       const uint32_t bar = smem_u32(bars + kb % NB);
       const int buf = (int)(kb % NB);
@@ -675,13 +675,13 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
     };
     // lanes [0, GPW) of warp w issue groups GPW w + lane (EARLY: the phase-1
     // warps only — they refill their single buffer right after gathering from
-    // it; ISSUE2: the phase-2 warps)
-    constexpr int NWI = ISSUE2 ? C::NW2 : EARLY ? C::NW1 : (C::NW < NG ? C::NW : NG);
+    // it.  Measured and rejected: the phase-2 warps refilling it after an
+    // mbarrier hand-over from phase 1, 11.2K / 15.2K MLUPS with the refill
+    // after / before their collision, against 16.0-16.3K)
+    constexpr int NWI = EARLY ? C::NW1 : (C::NW < NG ? C::NW : NG);
     constexpr int GPW = (NG + NWI - 1) / NWI;
-    const int wi = ISSUE2 ? warp - C::NW1 : warp;
-    const int my_grp = GPW * wi + (tid & 31);
-    const bool issuer = wi >= 0 && wi < NWI && (tid & 31) < GPW && my_grp < NG;
-    const uint32_t bar_gath = smem_u32(bars + NB + 4);
+    const int my_grp = GPW * warp + (tid & 31);
+    const bool issuer = warp < NWI && (tid & 31) < GPW && my_grp < NG;
 
     if (issuer)
       for (int k = 0; k < (EARLY ? NB : PF) && k < nload; ++k) issue_one(k, my_grp);
@@ -692,7 +692,12 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
       if (l2_dist > 0 && t + l2_dist < nload) {
         // L2 prefetch (LSU, not the TMA queue) of the newest column the loads
         // of iteration t + l2_dist touch: rows [ya - 6, ya + HT + 6) of all 37
-        // planes, 8 lines of 128 B each; N > 1: slab columns only
+        // planes, 8 lines of 128 B each; N > 1: slab columns only.  (A TMA
+        // L2 prefetch of the whole window — cp.async.bulk.prefetch.tensor, one
+        // instruction — measured 13.5K MLUPS at distance 2 down to 10.3K at
+        // 16 against 15.9K without, and 2 of ~10 such runs differed from the
+        // one-step kernel after 1000 steps, never reproduced with the loads
+        // synchronised per launch; not kept.)
         const int j = xs + t + l2_dist;  // c1(t + l2_dist) + 3
         if (!peers || j < lx + H) {
           const double* col = Asrc + (int64_t)(peers ? j : wrap_col(j, lx)) * g.cs + (rbase - 6);
@@ -708,7 +713,7 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
           // phase 1: state n+1 at column c1 = xs - 3 + t, rows [ya-3, ya+HT+3)
           const uint32_t kb = kglob + (uint32_t)t;
           const int buf = (int)(kb % NB);
-          mbar_wait(smem_u32(bars + buf), (kb / NB) & 1);
+          if (!LB_TB_NOLOAD) mbar_wait(smem_u32(bars + buf), (kb / NB) & 1);
           // wall strips: warp 0 fills the virtual rows (one copy per lane),
           // then the phase-1 warps meet at named barrier 1 before reading
           if (vbottom || vtop) {
@@ -737,12 +742,8 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
             // with iteration t + NB's windows while the collisions run
             double f[Q];
             phase1_gather<BUFD, RB>(s0, buf, valid ? i : 0, f);
-            if (ISSUE2) {  // buffer buf read: the phase-2 issuers may refill it
-              asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar_gath + 8 * buf) : "memory");
-            } else {
-              asm volatile("bar.sync 2, %0;" ::"r"(32 * C::NW1) : "memory");
-              if (issuer && t + NB < nload) issue_one(t + NB, my_grp);
-            }
+            asm volatile("bar.sync 2, %0;" ::"r"(32 * C::NW1) : "memory");
+            if (issuer && t + NB < nload) issue_one(t + NB, my_grp);
             if (NBAR) {
               if (valid) phase1_collide<COLL, MON>(f, y, ly, thermal, r, own, acc);
               if (t > 0) asm volatile("bar.sync %0, %1;" ::"r"(5 + ((t - 1) & 1)), "r"(C::NT) : "memory");
@@ -779,27 +780,6 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
         double f[Q];
         if (t >= 7) phase2_gather<R1>(s1, t, valid ? i : 0, f);
         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar_empty + 8 * (I & 1)) : "memory");
-        if (ISSUE2 && issuer && t + NB < nload) {  // see the ISSUE2 branch below
-          const uint32_t kb = kglob + (uint32_t)t;
-          mbar_wait(bar_gath + 8 * (kb % NB), (kb / NB) & 1);
-          issue_one(t + NB, my_grp);
-        }
-        if (valid)
-          phase2_update<COLL, MON>(f, B, g, y, xs - 7 + t, thermal, r, y >= own_lo && y < own_hi, acc, !peers);
-      } else if (ISSUE2) {
-        // phase 2: state n+2 at column c2 = xs - 7 + t, rows [ya, ya+HT);
-        // after its gather, the issuing lanes wait until phase 1 gathered from
-        // this iteration's state-n buffer and refill it with iteration t + NB's
-        const int i = tid - 32 * C::NW1;
-        const int y = ya + i;
-        const bool valid = t >= 7 && i < HT && y < ly;
-        double f[Q];
-        if (t >= 7) phase2_gather<R1>(s1, t, valid ? i : 0, f);
-        if (issuer && t + NB < nload) {
-          const uint32_t kb = kglob + (uint32_t)t;
-          mbar_wait(bar_gath + 8 * (kb % NB), (kb / NB) & 1);
-          issue_one(t + NB, my_grp);
-        }
         if (valid)
           phase2_update<COLL, MON>(f, B, g, y, xs - 7 + t, thermal, r, y >= own_lo && y < own_hi, acc, !peers);
       } else if (t >= 7) {
@@ -923,6 +903,8 @@ cudaError_t launch_tb(const Geo& g, const TbMaps* t, int src_buf, double* B, con
 }  // namespace
 
 bool tb_layout_ok(int ly) { return ly <= TB_HT || ly >= TB_HT + 6; }
+
+int tb_strip_height() { return TB_HT; }
 
 int tb_grid(const Geo& g, int grid) {
   const int64_t U = (int64_t)((g.ly + TB_HT - 1) / TB_HT) * g.lx;

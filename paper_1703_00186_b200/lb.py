@@ -29,7 +29,7 @@ EXPORTS = ["lb_query_layout", "lb_exchange_plan", "lb_constants", "lb_kwall", "l
            "lb_strerror", "lb_init", "lb_destroy", "lb_get_layout", "lb_set_stream", "lb_init_macro", "lb_init_rt",
            "lb_set_state", "lb_exchange", "lb_propagate", "lb_bc", "lb_collide", "lb_step",
            "lb_gather", "lb_peek", "lb_invariants", "lb_sync", "lb_profile_enable",
-           "lb_profile_reset", "lb_profile_read", "lb_launch_count", "lb_set_peers",
+           "lb_profile_reset", "lb_profile_read", "lb_launch_count", "lb_tb_strip_height", "lb_set_peers",
            "lb_monitor", "lb_peek_cols", "lb_set_option", "lb_invariants_async", "lb_invariants_pair_async"]
 
 
@@ -121,6 +121,7 @@ def lib():
         "lb_profile_enable": (i, [vp, i]), "lb_profile_reset": (i, [vp]),
         "lb_profile_read": (i, [vp, p(lb_kprof), i, p(i)]),
         "lb_launch_count": (ctypes.c_int64, [vp]),
+        "lb_tb_strip_height": (i, []),
         "lb_set_peers": (i, [vp, p(lb_peers)]),
         "lb_monitor": (i, [vp, i]),
         "lb_set_option": (i, [vp, i, i]),
@@ -153,6 +154,11 @@ def constants():
     t0 = ctypes.c_double()
     _check(lib().lb_constants(c.ctypes.data_as(ctypes.c_void_p), _dptr(w), ctypes.byref(a), ctypes.byref(t0)))
     return c.reshape(Q, 2).astype(np.int64), w, a.value, t0.value
+
+
+def tb_strip_height() -> int:
+    """Strip height HT of the library's two-step kernel (lb_tb_strip_height)."""
+    return int(lib().lb_tb_strip_height())
 
 
 def t0() -> float:
@@ -445,14 +451,15 @@ class Lattice:
         """Replay 2-step CUDA graphs in lb_step (needs a non-default stream)."""
         _check(lib().lb_set_option(self._ctx, 2, int(enable)))
 
-    def temporal(self, enable: bool = True, grid: int = 0, l2_prefetch: int = 0, wall_weight16: int = 20,
+    def temporal(self, enable: bool = True, grid: int = 0, l2_prefetch: int = 0, wall_weight16: int = 0,
                  l2_promotion: int | None = None):
         """Two steps per pass over HBM (LB_OPT_TEMPORAL, the default where it
         applies: fused mode, walls, N = 1 or N > 1 in peer mode, monitors on or
         off — with monitors the kernel reduces both states' invariants):
         lb_step advances pairs of steps with the two-step kernel.  grid: CTAs
         (0 = one per SM); l2_prefetch: L2 prefetch distance in columns (0 = off);
-        wall_weight16: cost of a wall-strip column, x16, for the work split;
+        wall_weight16: cost of a wall-strip column, x16, for the work split
+        (0 = the library default: 19 BGK, 20 regularised);
         l2_promotion: L2 promotion of its TMA loads in bytes (None = library default)."""
         _check(lib().lb_set_option(self._ctx, 3, int(enable)))
         _check(lib().lb_set_option(self._ctx, 4, int(grid)))

@@ -702,25 +702,26 @@ def test_tma_fused_step_bit_identical(lb, coll, bc, shape):
 
 # ------------------------------------------------------------------ two steps per pass (temporal blocking)
 
-TB_HT = 104   # strip height of the shipped two-step kernel (lb_tb.cu LB_TB_HT)
+TB_HT = 104   # strip height of the shipped two-step kernel (lb_tb.cu LB_TB_HT; test_lib_host pins it)
 
 
 @pytest.mark.parametrize("coll", ["bgk", "regularized"])
 @pytest.mark.parametrize("bc", ["thermal", "adiabatic"])
 @pytest.mark.parametrize("shape", [(6, 6), (24, 40), (17, 131), (64, 32), (9, 300), (131, 200), (12, 60),
-                                   # the strip-layout edges of HT = 104 (strip_ya / tb_layout_ok):
-                                   (10, 104), (9, 105), (8, 107), (7, 109), (11, 110), (9, 111),
-                                   (9, 208), (13, 214), (9, 215), (8, 312), (7, 318)])
+                                   # the strip-layout edges of HT (strip_ya / tb_layout_ok):
+                                   (10, TB_HT), (9, TB_HT + 1), (8, TB_HT + 3), (7, TB_HT + 5),
+                                   (11, TB_HT + 6), (9, TB_HT + 7), (9, 2 * TB_HT), (13, 2 * TB_HT + 6),
+                                   (9, 2 * TB_HT + 7), (8, 3 * TB_HT), (7, 3 * TB_HT + 6)])
 def test_two_step_kernel_bit_identical(lb, coll, bc, shape):
     """LB_OPT_TEMPORAL (k_step2_tb: states n+1 and n+2 in one pass, n+1 kept in
     shared memory) == two one-step fused launches bit for bit, and both == the
-    oracle (<= 1e-12).  Shapes around the shipped strip height HT = 104:
-    exactly one strip (104), the band 105..109 where no strip layout keeps the
-    wall bands inside wall strips (lb_step must fall back to the one-step
-    kernel — asserted from the launch names), the moved second strip (110,
-    111), two exact strips (208) plus 6 / 7 rows (214, 215), three strips
-    (312, 318); sweeps that wrap periodically in x, CTA ranges that cross strip
-    boundaries; odd step counts end with one fused step."""
+    oracle (<= 1e-12).  Shapes around the shipped strip height HT: exactly one
+    strip (HT), the band HT+1..HT+5 where no strip layout keeps the wall bands
+    inside wall strips (lb_step must fall back to the one-step kernel —
+    asserted from the launch names), the moved second strip (HT+6, HT+7), two
+    exact strips (2 HT) plus 6 / 7 rows, three strips (3 HT, 3 HT + 6); sweeps
+    that wrap periodically in x, CTA ranges that cross strip boundaries; odd
+    step counts end with one fused step."""
     lx, ly = shape
     st = oracle_state(lx, ly, seed=lx * 7 + ly)
     grav = (1e-6, -1e-5)

@@ -119,3 +119,10 @@ def test_oracle_and_library_share_no_code():
             if fn.endswith((".cu", ".cuh", ".h", ".py")):
                 s = open(os.path.join(dirpath, fn)).read()
                 assert not bad_in_pkg.search(s), fn
+
+
+def test_two_step_strip_height_matches_the_gpu_tests():
+    """The strip-layout edge shapes of tests/test_gpu_parity.py are derived
+    from TB_HT there; the library reports the height it was built with."""
+    import test_gpu_parity
+    assert lb.tb_strip_height() == test_gpu_parity.TB_HT

@@ -19,7 +19,7 @@ def main():
     ht, pf = int(sys.argv[1]), int(sys.argv[2])
     early = int(sys.argv[3]) if len(sys.argv) > 3 else 0
     extra = sys.argv[4:]  # further NAME=VALUE defines, e.g. LB_TB_DECOUPLE=1
-    tag = f"ht{ht}_pf{pf}" + (f"_e{early}" if early else "") + "".join(
+    tag = os.environ.get("TB_TAG", "") + f"ht{ht}_pf{pf}" + (f"_e{early}" if early else "") + "".join(
         "_" + d.split("=")[0].replace("LB_TB_", "").lower() + d.split("=")[1] for d in extra)
     _build.build()
     nd = _build.nccl_dir()
@@ -28,9 +28,9 @@ def main():
     obj = os.path.join(out, f"lb_tb_{tag}.o")
     flags = [_build.ARCH, "-O3", "-lineinfo", "-std=c++17", "--fmad=false", "--expt-relaxed-constexpr",
              "-Xcompiler", "-fPIC,-ffp-contract=off,-fno-fast-math", "-Xptxas", "-v,-warn-spills",
-             "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nd, "include"),
+             "-I", os.path.join(ROOT, "include"), "-I", os.path.join(_build.HERE, "csrc"), "-I", os.path.join(nd, "include"),
              f"-DLB_TB_HT={ht}", f"-DLB_TB_PF={pf}", f"-DLB_TB_EARLY={early}", *("-D" + d for d in extra)]
-    src = os.path.join(_build.HERE, "csrc", "lb_tb.cu")
+    src = os.environ.get("TB_SRC") or os.path.join(_build.HERE, "csrc", "lb_tb.cu")  # TB_SRC: e.g. an older revision
     r = subprocess.run(["nvcc", *flags, "-c", src, "-o", obj], capture_output=True, text=True)
     sys.stdout.write("\n".join(l for l in (r.stdout + r.stderr).splitlines()
                                if "k_step2_tb" in l or "registers" in l or "spill" in l or "error" in l))

@@ -17,7 +17,7 @@ import lbgen  # noqa: E402
 import paper_1703_00186_b200 as lbm  # noqa: E402
 
 
-def run(lx, ly, tb, grid=0, l2=0, k=None, coll="bgk", ww=20, promo=None):
+def run(lx, ly, tb, grid=0, l2=0, k=None, coll="bgk", ww=0, promo=None):
     k = k or int(os.environ.get("TB_K", "200"))
     s = torch.cuda.Stream()
     g = lbm.Lattice(lx, ly, collision=coll, stream=s, temporal=False)
@@ -44,8 +44,8 @@ def main():
     ms, ml, ref = run(lx, ly, False)
     res.append({"tb": 0, "ms_per_step": ms, "mlups": ml})
     print(json.dumps(res[-1]), flush=True)
-    grids = [int(x) for x in os.environ.get("TB_GRIDS", "0,296").split(",")]
-    l2s = [int(x) for x in os.environ.get("TB_L2", "0,2,4,8").split(",")]
+    grids = [int(x) for x in os.environ.get("TB_GRIDS", "0,296").split(",") if x]
+    l2s = [int(x) for x in os.environ.get("TB_L2", "0,2,4,8").split(",") if x]
     for grid in grids:
         for l2 in l2s:
             ms, ml, out = run(lx, ly, True, grid, l2)

@@ -30,7 +30,7 @@ import lbgen  # noqa: E402
 import paper_1703_00186_b200 as lb  # noqa: E402
 from paper_1703_00186_b200 import perfmodel as pm  # noqa: E402
 
-HT = 104
+HT = lb.tb_strip_height()
 
 
 def n1_launch_ms(lx, ly, pairs=20):
