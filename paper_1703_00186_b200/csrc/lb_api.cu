@@ -152,6 +152,7 @@ struct lb_ctx {
   int tb_wall_w16 = 0;          // LB_OPT_TB_WALL_WEIGHT: wall-strip column cost x16 (work split; 0 = per collision)
   int tb_edge_pull = 1;         // LB_OPT_TB_EDGE_PULL: N > 1 two-step exchange inside the kernel (1) or k_tb_pull first (0)
   double* d_stage = nullptr;    // N > 1 two-step: the neighbours' 6 edge columns (2 x 6 x cs doubles)
+  unsigned int* d_ctas = nullptr;  // N > 1 two-step, in-kernel exchange: finished-CTA count (kept zero)
   double* d_mon_tb = nullptr;   // two-step monitors: 2 x cap x 5 per-CTA partials, then reduce scratch
   int mon_tb_cap = 0;           // CTAs d_mon_tb holds partials for
   int mon_tb_G = 0;             // CTAs of the last two-step launch
@@ -651,6 +652,7 @@ void lb_destroy(lb_ctx* c) {
   if (c->d_mon) cudaFree(c->d_mon);
   if (c->d_mon_tb) cudaFree(c->d_mon_tb);
   if (c->d_stage) cudaFree(c->d_stage);
+  if (c->d_ctas) cudaFree(c->d_ctas);
   if (c->d_ticket) cudaFree(c->d_ticket);
   if (c->d_status) cudaFree(c->d_status);
   if (c->d_nonphys) cudaFree(c->d_nonphys);
@@ -875,14 +877,12 @@ static int step_tb(lb_ctx* c) {
   const lb_peers& P = c->peers;
   const bool peers = c->peers_on;
   lbk::TbPeer pull;
-  const bool inpull = peers && c->tb_edge_pull;
-  if (inpull) {  // N > 1 default: only the edge CTAs wait and stage (overlapped with the interior)
-    pull.L = P.left_buf[c->par];
-    pull.R = P.right_buf[c->par];
-    pull.stage = c->d_stage;
+  const bool inpull = peers && c->tb_edge_pull && c->tb->direct;
+  if (inpull) {  // N > 1 default: only the edge CTAs wait; the kernel reads the neighbours' buffers and signals
     pull.waitL = reinterpret_cast<const unsigned long long*>(P.left_done);
     pull.waitR = reinterpret_cast<const unsigned long long*>(P.right_done);
-    pull.my_done = reinterpret_cast<const unsigned long long*>(P.my_done);
+    pull.my_done = reinterpret_cast<unsigned long long*>(P.my_done);
+    pull.ctas_done = c->d_ctas;
     pull.status = c->d_status;
     pull.timeout_ns = c->peer_timeout_ns;
   } else if (peers) {  // LB_OPT_TB_EDGE_PULL = 0: wait for both neighbours, copy their 6 edge columns, then the kernel
@@ -901,9 +901,10 @@ static int step_tb(lb_ctx* c) {
   }));
   if (peers) {  // publish: this launch is complete (the neighbours may now read our new state)
     c->peer_step += 1;
-    TRY(launch(c, "k_signal", c->s, 0, [&] {
-      return lbk::launch_signal(reinterpret_cast<unsigned long long*>(P.my_done), c->s);
-    }));
+    if (!inpull)  // (the in-kernel exchange publishes from the kernel's last CTA)
+      TRY(launch(c, "k_signal", c->s, 0, [&] {
+        return lbk::launch_signal(reinterpret_cast<unsigned long long*>(P.my_done), c->s);
+      }));
   }
   swap_ab(c);  // B held state n + 2: it becomes A
   // N = 1: the kernel stored the border columns into B's halo; N > 1: halos
@@ -1120,11 +1121,19 @@ int lb_set_peers(lb_ctx* c, const lb_peers* p) {
     return fail(LB_ENOMEM, "status allocation failed");
   CU(cudaMemsetAsync(c->d_status, 0, sizeof(unsigned int), c->s));
   if (const char* e = std::getenv("LB_PEER_TIMEOUT_MS")) c->peer_timeout_ns = 1000000ull * std::strtoull(e, nullptr, 10);
-  // two-step kernel at N > 1: staging for the neighbours' edge columns
-  if (c->tb && !c->tb->staged) {
-    if (!c->d_stage && cudaMalloc(&c->d_stage, (size_t)12 * c->g.cs * sizeof(double)) != cudaSuccess)
-      return fail(LB_ENOMEM, "staging allocation failed");
-    if (!lbk::tb_attach_staging(c->tb, c->g, c->d_stage)) return fail(LB_ECUDA, "staging tensor maps failed");
+  // two-step kernel at N > 1: tensor maps of the neighbours' buffers (the
+  // in-kernel exchange), and staging for the neighbours' edge columns (the
+  // k_tb_pull path: LB_OPT_TB_EDGE_PULL = 0, or maps the driver refuses)
+  if (c->tb) {
+    if (!c->tb->staged) {
+      if (!c->d_stage && cudaMalloc(&c->d_stage, (size_t)12 * c->g.cs * sizeof(double)) != cudaSuccess)
+        return fail(LB_ENOMEM, "staging allocation failed");
+      if (!lbk::tb_attach_staging(c->tb, c->g, c->d_stage)) return fail(LB_ECUDA, "staging tensor maps failed");
+    }
+    lbk::tb_attach_peers(c->tb, c->g, p->left_buf, p->right_buf);  // false: the kernel falls back to k_tb_pull
+    if (!c->d_ctas && cudaMalloc(&c->d_ctas, sizeof(unsigned int)) != cudaSuccess)
+      return fail(LB_ENOMEM, "CTA counter allocation failed");
+    CU(cudaMemsetAsync(c->d_ctas, 0, sizeof(unsigned int), c->s));
   }
   c->peers = *p;
   c->peers_on = true;

@@ -88,6 +88,9 @@ cudaError_t launch_step_fused_tma(const Geo& g, const TmaMaps* t, int src_buf, c
 struct TbMaps {
   CUtensorMap load[2][3];  // column-group windows, box {HT + 12, 3 | 5 | 7, 1}, per buffer
   CUtensorMap st[2][3];    // N > 1: staging of the left / right neighbour's 6 edge columns
+  CUtensorMap nb[2][2][3]; // N > 1: the left (0) / right (1) neighbour's buffer k, read directly (tb_attach_peers)
+  bool direct = false;     // nb[] encoded
+  double* nbuf[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // the buffers nb[] describes
   bool staged = false;  // st[] encoded (tb_attach_staging)
   int promo = 0;        // L2 promotion of every map: 0 / 64 / 128 / 256 bytes (LB_OPT_TB_L2_PROMOTION)
   double* bufs[2] = {nullptr, nullptr};
@@ -100,6 +103,11 @@ bool tb_set_promotion(TbMaps* t, const Geo& g, int promo);
 // neighbour's last 6 physical columns (our internal columns -3..2), [6 cs,
 // 12 cs) the right neighbour's first 6 (our internal lx+3..lx+8)
 bool tb_attach_staging(TbMaps* t, const Geo& g, double* stage);
+// N > 1 (peer mode): tensor maps of the neighbours' two buffers (same layout
+// as ours: equal slabs), so the kernel's edge CTAs load the columns beyond the
+// slab straight from the neighbours' current buffer; false if the driver
+// cannot encode them (peer mapping), the caller then stages (k_tb_pull)
+bool tb_attach_peers(TbMaps* t, const Geo& g, double* const left[2], double* const right[2]);
 // Fill the staging buffer from the neighbours' current buffers (peer memory)
 // once both have completed as many launches as this rank (*waitL/R >= *my_done;
 // watchdog: *status = 1 after timeout_ns, 0 = wait forever).
@@ -119,13 +127,16 @@ cudaError_t tb_upload_constants(const double* k_bottom, const double* k_top, con
 // this rank, then copy the rows of the neighbour's 6 edge columns their strip
 // needs into the staging buffer themselves; every other CTA starts at once,
 // so the exchange overlaps the interior sweeps (§8a6).
+// N > 1, exchange inside the two-step kernel: the edge CTAs wait for the
+// neighbours' launch counters (watchdog: status, timeout_ns) and load the
+// columns beyond the slab from the neighbours' current buffers (TbMaps::nb);
+// the last CTA to finish publishes this rank's counter (my_done += 1) —
+// ctas_done counts finished CTAs and is reset by that last CTA.
 struct TbPeer {
-  const double* L = nullptr;   // left neighbour's current buffer (peer memory)
-  const double* R = nullptr;   // right neighbour's current buffer
-  double* stage = nullptr;     // tb_attach_staging's buffer
   const unsigned long long* waitL = nullptr;
   const unsigned long long* waitR = nullptr;
-  const unsigned long long* my_done = nullptr;
+  unsigned long long* my_done = nullptr;
+  unsigned int* ctas_done = nullptr;
   unsigned int* status = nullptr;
   unsigned long long timeout_ns = 0;
 };

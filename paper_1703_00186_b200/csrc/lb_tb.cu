@@ -495,22 +495,6 @@ __device__ __forceinline__ void peer_wait(const unsigned long long* a, const uns
   }
 }
 
-// Rows [r0, r0 + RB) of the 6 staged columns of one side (all 37 populations),
-// clipped to the nyp rows of a population column (the TMA box zero-fills rows
-// beyond it): src = the neighbour's first staged column, dst = that side's
-// staging block.  r0 and nyp are even: 16-byte moves.
-template <int RB, int NT>
-__device__ __forceinline__ void edge_copy(double* __restrict__ dst, const double* src, int64_t cs, int nyp, int r0) {
-  const int n2 = (min(RB, nyp - r0)) / 2;  // double2 per population column
-  const int per_col = Q * n2;
-  for (int q = threadIdx.x; q < 6 * per_col; q += NT) {
-    const int col = q / per_col, rem = q - col * per_col;
-    const int l = rem / n2, k = rem - l * n2;
-    const int64_t off = col * cs + (int64_t)l * nyp + r0 + 2 * k;
-    *reinterpret_cast<double2*>(dst + off) = __ldcg(reinterpret_cast<const double2*>(src + off));
-  }
-}
-
 template <int COLL, int HT, int PF, bool MON>
 __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
     k_step2_tb(const __grid_constant__ TbKMaps km, double* __restrict__ B, Geo g, Relax r, int nstrips,
@@ -622,23 +606,21 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
     const bool vbottom = ya - 3 < 3;
     const bool vtop = ya + HT + 3 > ly - 3;
 
-    // N > 1, in-kernel edge pulls: this sweep reads state-n columns [x0 - 6,
-    // x1 + 6) and writes [x0, x1).  Within 6 columns of the left edge it reads
-    // the left neighbour's last columns (complete once its previous launch
-    // is) and overwrites columns the neighbour's previous launch pulled: wait
-    // for its counter, then stage this strip's rows of its 6 edge columns.
-    // Same on the right.  Interior sweeps never wait.
+    // N > 1, exchange inside the kernel: this sweep reads state-n columns
+    // [x0 - 6, x1 + 6) and writes [x0, x1).  Within 6 columns of the left
+    // edge it reads the left neighbour's last columns (final once its previous
+    // launch completed) and overwrites columns that neighbour's previous
+    // launch read: wait for its counter, then the TMA loads those columns
+    // straight from its current buffer.  Same on the right.  Interior sweeps
+    // never wait.
     if (inpull) {
       const bool needL = x0 < 6, needR = x1 > lx - 6;
       if (needL || needR) {  // CTA-uniform
         if (tid == 0) peer_wait(needL ? pp.waitL : nullptr, needR ? pp.waitR : nullptr, pp.my_done, pp.status,
                                 pp.timeout_ns);
         __syncthreads();
-        if (needL) edge_copy<RB, C::NT>(pp.stage, pp.L + (int64_t)(lx - 3) * g.cs, g.cs, g.nyp, rbase - 6);
-        if (needR) edge_copy<RB, C::NT>(pp.stage + 6 * g.cs, pp.R + 3 * g.cs, g.cs, g.nyp, rbase - 6);
-        // generic-proxy global writes, read next by this CTA's TMA (async proxy)
+        // the neighbours' generic-proxy stores (other kernels), read next by this CTA's TMA
         asm volatile("fence.proxy.async.global;" ::: "memory");
-        __syncthreads();
       }
     }
 
@@ -661,12 +643,14 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
       const double* dst = s0 + buf * BUFD + gp.z;
       // source column: N = 1 periodic wrap; N > 1 the staging buffers beyond
       // the slab (left: internal -3..2, right: lx+3..lx+8)
+      // (in-kernel exchange: the neighbours' buffers, whose internal column
+      // lx + j resp. j - lx is our column j; staged: the staging buffers)
       const int j = c1 - gp.w;
       const CUtensorMap* m = &km.src[cls];
       int col = j;
       if (!peers) col = wrap_col(j, lx);
-      else if (j < H) { m = &km.stL[cls]; col = j + H; }
-      else if (j >= lx + H) { m = &km.stR[cls]; col = j - lx - H; }
+      else if (j < H) { m = &km.stL[cls]; col = inpull ? j + lx : j + H; }
+      else if (j >= lx + H) { m = &km.stR[cls]; col = inpull ? j - lx : j - lx - H; }
       asm volatile(
           "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
           " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
@@ -801,6 +785,21 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
     iglob += (uint32_t)niter;
     __syncthreads();  // the next sweep refills every ring
   }
+  if (inpull) {
+    // publish this launch (the neighbours may now read our new state and
+    // overwrite the columns we read): the last CTA to finish, after every
+    // CTA's stores, raises this rank's counter (system-scope release)
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence_system();
+      if (atomicAdd(pp.ctas_done, 1u) == gridDim.x - 1) {
+        __threadfence_system();
+        *pp.ctas_done = 0u;  // for the next launch (stream order)
+        const unsigned long long v = *pp.my_done + 1;
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(pp.my_done), "l"(v) : "memory");
+      }
+    }
+  }
 #if LB_TB_CLOCK
   if (tid == 0 && blockIdx.x < 1024) {
     unsigned long long clk1;
@@ -886,17 +885,18 @@ cudaError_t launch_tb(const Geo& g, const TbMaps* t, int src_buf, double* B, con
     if (e != cudaSuccess) return e;
     if (dev < 64) done_mask |= 1ull << dev;
   }
-  if (peers && !t->staged) return cudaErrorInvalidValue;
+  const bool inpull = peers && pull;
+  if (peers && !(inpull ? t->direct : t->staged)) return cudaErrorInvalidValue;
   TbKMaps km;
   for (int c = 0; c < 3; ++c) {
     km.src[c] = t->load[src_buf][c];
-    km.stL[c] = peers ? t->st[0][c] : t->load[src_buf][c];
-    km.stR[c] = peers ? t->st[1][c] : t->load[src_buf][c];
+    km.stL[c] = !peers ? t->load[src_buf][c] : inpull ? t->nb[0][src_buf][c] : t->st[0][c];
+    km.stR[c] = !peers ? t->load[src_buf][c] : inpull ? t->nb[1][src_buf][c] : t->st[1][c];
   }
-  const TbPeer pp = (peers && pull) ? *pull : TbPeer{};
+  const TbPeer pp = inpull ? *pull : TbPeer{};
   kern<<<tb_grid(g, grid), Cfg::NT, Cfg::SMEM, s>>>(km, B, g, r, (g.ly + TB_HT - 1) / TB_HT, l2_dist, thermal,
                                                     wall_w16, mon, peers, t->bufs[src_buf], pp,
-                                                    (peers && pull) ? 1 : 0);
+                                                    inpull ? 1 : 0);
   return cudaGetLastError();
 }
 
@@ -936,6 +936,7 @@ TbMaps* tb_create(const Geo& g, double* buf0, double* buf1, int promo) {
 bool tb_set_promotion(TbMaps* t, const Geo& g, int promo) {
   t->promo = promo;
   if (!encode_buffers(t, g)) return false;
+  if (t->direct && !tb_attach_peers(t, g, t->nbuf[0], t->nbuf[1])) return false;
   return !t->staged || tb_attach_staging(t, g, t->stage);
 }
 
@@ -999,6 +1000,19 @@ bool tb_attach_staging(TbMaps* t, const Geo& g, double* stage) {
   t->stage = stage;
   t->staged = true;
   return true;
+}
+
+bool tb_attach_peers(TbMaps* t, const Geo& g, double* const left[2], double* const right[2]) {
+  for (int k = 0; k < 2; ++k)
+    for (int c = 0; c < 3; ++c)
+      if (!encode(&t->nb[0][k][c], left[k], g, Cfg::RB, CLS_N[c], t->promo) ||
+          !encode(&t->nb[1][k][c], right[k], g, Cfg::RB, CLS_N[c], t->promo))
+        return t->direct = false;
+  t->nbuf[0][0] = left[0];
+  t->nbuf[0][1] = left[1];
+  t->nbuf[1][0] = right[0];
+  t->nbuf[1][1] = right[1];
+  return t->direct = true;
 }
 
 cudaError_t launch_tb_pull(const Geo& g, double* stage, const double* left_A, const double* right_A,

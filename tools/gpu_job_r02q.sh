@@ -8,3 +8,4 @@ timeout 900 python tools/timing_model_tb.py --out $O/r02_timing_model.json > $O/
 timeout 1500 python tests/long_run.py --lx 2048 --ly 4096 --nslabs 8 --compare-n1 --steps 10000 --every 100 --ckpt-every 1000 --check 10 --out $O/r02_long_run_n8.json > $O/lr.log 2>&1; tail -2 $O/lr.log | cut -c1-1200
 timeout 1200 python tools/drift_study.py --lx 256 --ly 4096 --steps 1000 --every 100 --side both --out $O/r02_drift_study.json > $O/drift.log 2>&1; tail -4 $O/drift.log | cut -c1-800
 timeout 300 python tools/fp64_bench.py --out $O/r02_fp64_hbm_microbench.json > $O/fp64.log 2>&1; tail -3 $O/fp64.log | cut -c1-600
+timeout 2400 python -m pytest tests -m gpu -q --timeout 900 > $O/gpu_tests.log 2>&1; tail -3 $O/gpu_tests.log

@@ -102,7 +102,8 @@ def main():
             d = {"k_step2_tb_ms": kt["total_ms"] / kt["launches"]}
             if "k_tb_pull" in pr:
                 d["k_tb_pull_ms"] = pr["k_tb_pull"]["total_ms"] / pr["k_tb_pull"]["launches"]
-            d["k_signal_ms"] = pr["k_signal"]["total_ms"] / pr["k_signal"]["launches"]
+            # (the in-kernel exchange publishes from the kernel: no k_signal)
+            d["k_signal_ms"] = pr["k_signal"]["total_ms"] / pr["k_signal"]["launches"] if "k_signal" in pr else 0.0
             d["launch_sum_ms"] = d["k_step2_tb_ms"] + d.get("k_tb_pull_ms", 0.0) + d["k_signal_ms"]
             per_rank.append(d)
         got = np.concatenate([g.peek(0) for g in ranks], axis=1)

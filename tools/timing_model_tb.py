@@ -8,13 +8,14 @@ and stage, the default).  Predicts N = 8 efficiencies of BASELINE configs #3
 
 Per launch of 2 steps on n GPUs (slab lx = Lx/n):
     T_ser(n)  = alpha2 lx Ly + beta2 lx + [n > 1] (T_pull(Ly) + T_sig)
-    T_ovl(n)  = alpha2 lx Ly + beta2 lx + [n > 1] (T_edge(Ly) + T_sig)
+    T_ovl(n)  = alpha2 lx Ly + beta2 lx + [n > 1] T_edge(Ly)
 alpha2, beta2: least squares over k_step2_tb launches at N = 1 (CUDA events);
 T_pull: the k_tb_pull launch of an in-process ring on this GPU (its copy is
 local here) or the NVLink time of its bytes, whichever is larger; T_edge:
 the extra per-launch time of the in-kernel edge pull measured on the same
 ring (shared stream, each launch alone on the GPU) plus the NVLink time of one
-edge CTA's 6-column rows; T_sig: the k_signal launch.  The pool has one GPU,
+edge CTA's 6-column rows; T_sig: the k_signal launch (serialised path only:
+the in-kernel exchange publishes its counter from the kernel's last CTA).  The pool has one GPU,
 so the NVLink terms are inputs (B200_PROFILING.md's peer-copy rate), not
 measurements.
 """
@@ -118,7 +119,9 @@ def main():
         t = (alpha2 * lx_slab * ly + beta2 * lx_slab) * 1e3
         if n > 1:
             e = terms(ly)
-            t += (e["T_pull_ms"] if mode == "serialised" else e["T_edge_ms"]) + e["T_sig_ms"]
+            # serialised: k_tb_pull + kernel + k_signal; in-kernel: the edge
+            # CTAs' waits and peer reads, and the kernel's last CTA signals
+            t += e["T_pull_ms"] + e["T_sig_ms"] if mode == "serialised" else e["T_edge_ms"]
         return t
 
     pred = {}
