@@ -140,6 +140,70 @@ LB_HD constexpr int GOFF(int g, int RB) {
 // offset of population l's window (row ya - 6) in a state-n buffer
 LB_HD constexpr int POFF(int l, int RB) { return GOFF(GOF(l), RB) + (l - GFIRST(GOF(l))) * RB; }
 
+// ---- TMEM-resident state-(n+1) ring (LB_TB_TMEM) ----------------------------
+// Phase 1 writes state n+1 of its rows to a shared-memory staging buffer, two
+// populations of equal cy per 16-byte row ("pairs": each cy group in label
+// order, i.e. cx descending, paired off, 22 pairs); one thread then copies
+// every pair into the ring in tensor memory with tcgen05.cp .128x128b from a
+// descriptor whose start is shifted by 3 - cy rows, so TMEM lane p receives
+// staging row p + 3 - cy — exactly the value phase 2 pulls for strip row p.
+// Phase 2 (lane quarter = its warp) reads its own lane with tcgen05.ld, so the
+// ±3-row pull costs no shared-memory traffic.  Pair j keeps TP_LT(j) =
+// cx_A + 5 slots of 4 columns (its first population has the larger cx): 440
+// of the 512 columns.  tools/tmem_probe.cu checks the shifted copy.
+constexpr int NPAIR = 22;
+LB_HD constexpr int TP_A(int j) {
+  constexpr int t[NPAIR] = {8, 22, 3, 16, 29, 0, 10, 24, 34, 1, 11, 25, 35, 2, 12, 26, 36, 7, 20, 33, 14, 28};
+  return t[j];
+}
+LB_HD constexpr int TP_B(int j) {  // -1: a single population
+  constexpr int t[NPAIR] = {15, -1, 9, 23, -1, 4, 17, 30, -1, 5, 18, 31, -1, 6, 19, 32, -1, 13, 27, -1, 21, -1};
+  return t[j];
+}
+LB_HD constexpr int TP_CY(int j) {
+  constexpr int t[NPAIR] = {-3, -3, -2, -2, -2, -1, -1, -1, -1, 0, 0, 0, 0, 1, 1, 1, 1, 2, 2, 2, 3, 3};
+  return t[j];
+}
+LB_HD constexpr int TP_LT(int j) {
+  constexpr int t[NPAIR] = {6, 4, 7, 5, 3, 8, 6, 4, 2, 8, 6, 4, 2, 8, 6, 4, 2, 7, 5, 3, 6, 4};
+  return t[j];
+}
+LB_HD constexpr int TP_COL(int j) {  // first TMEM column of pair j's slots
+  constexpr int t[NPAIR + 1] = {0,   24,  40,  68,  88,  100, 132, 156, 172, 180, 212, 236,
+                                252, 260, 292, 316, 332, 340, 368, 388, 400, 424, 440};
+  return t[j];
+}
+LB_HD constexpr int POP_PAIR(int l) {
+  constexpr int t[Q] = {5, 9,  13, 2,  5,  9,  13, 17, 0, 2,  6,  10, 14, 17, 20, 0,  3,  6, 10,
+                        14, 18, 20, 1, 3, 7, 11, 15, 18, 21, 4, 7, 11, 15, 19, 8, 12, 16};
+  return t[l];
+}
+LB_HD constexpr int POP_HALF(int l) {
+  constexpr int t[Q] = {0, 0, 0, 0, 1, 1, 1, 0, 0, 1, 0, 0, 0, 1, 0, 1, 0, 1, 1,
+                        1, 0, 1, 0, 1, 0, 0, 0, 1, 0, 0, 1, 1, 1, 0, 0, 0, 0};
+  return t[l];
+}
+constexpr bool tmem_tables_ok() {
+  int col = 0, seen = 0;
+  for (int j = 0; j < NPAIR; ++j) {
+    const int a = TP_A(j), b = TP_B(j);
+    if (TP_COL(j) != col || CY(a) != TP_CY(j) || TP_LT(j) != CX(a) + 5) return false;
+    if (POP_PAIR(a) != j || POP_HALF(a) != 0) return false;
+    ++seen;
+    if (b >= 0) {
+      if (CY(b) != TP_CY(j) || CX(b) >= CX(a) || POP_PAIR(b) != j || POP_HALF(b) != 1) return false;
+      ++seen;
+    }
+    col += 4 * TP_LT(j);
+  }
+  return seen == Q && TP_COL(NPAIR) == col && col <= 512;
+}
+static_assert(tmem_tables_ok(), "TMEM ring pair tables");
+
+#ifndef LB_TB_TMEM
+#define LB_TB_TMEM 0
+#endif
+
 template <int HT_, int PF_>
 struct TbCfg {
   static constexpr int HT = HT_;
@@ -153,9 +217,14 @@ struct TbCfg {
   static constexpr int NT = 32 * NW;
   static constexpr int NB = PF + 1;                 // state-n buffers per population = mbarriers
   static constexpr int S0_DBL = NB * BUFD;
-  static constexpr int S1_DBL = SLOTS1_BEFORE(Q) * R1;
+  // the state-(n+1) ring in shared memory, or (LB_TB_TMEM) two staging buffers
+  // of NPAIR pair regions of R1 rows x 16 bytes (+ 24 rows: the shifted copy
+  // of the last pair reads up to row 6 + 127)
+  static constexpr int STG_DBL = NPAIR * R1 * 2 + 48;
+  static constexpr int S1_DBL = LB_TB_TMEM ? 2 * STG_DBL : SLOTS1_BEFORE(Q) * R1;
   // mbarriers: NB TMA buffers + (LB_TB_DECOUPLE) 2 full + 2 empty ring barriers
-  static constexpr size_t SMEM = (size_t)(S0_DBL + S1_DBL) * sizeof(double) + (NB + 4) * sizeof(uint64_t);
+  // + (LB_TB_TMEM) 2 copy-complete barriers; then the TMEM base address
+  static constexpr size_t SMEM = (size_t)(S0_DBL + S1_DBL) * sizeof(double) + (NB + 6) * sizeof(uint64_t) + 16;
   static_assert(RB % 2 == 0 && RB <= 256, "TMA box rows");
   static_assert(SMEM <= 232448, "shared memory per CTA");
   static_assert(NW <= 8, "two warps per scheduler at most (64 KB register file per scheduler)");
@@ -426,6 +495,82 @@ __device__ __forceinline__ void phase2(const double* s1, double* __restrict__ B,
   phase2_update<COLL, MON>(f, B, g, y, c2, thermal, r, own, acc, wrap);
 }
 
+// ---- TMEM ring helpers (LB_TB_TMEM) ------------------------------------------
+// state n+1 of phase-1 row i (strip-relative, i = y - ya + 3) into staging row
+// i of every pair (16-byte stores; single populations 8 bytes), and the
+// mirrored values of the wall rows into the rows beyond the wall
+// (phase1_store's virtual rows, same rule)
+template <int R1>
+__device__ __forceinline__ void stage_store(const double (&f)[Q], double* stg, int i, int y, int ly) {
+  const int io = opaque(i);
+#pragma unroll
+  for (int j = 0; j < NPAIR; ++j) {
+    double* q = stg + 2 * (j * R1 + io);
+    if (TP_B(j) >= 0) *reinterpret_cast<double2*>(q) = make_double2(f[TP_A(j)], f[TP_B(j)]);
+    else q[0] = f[TP_A(j)];
+  }
+  if (y < 3 || y >= ly - 3) {
+    const int vi = y < 3 ? i - 2 * y - 1 : i + 2 * (ly - 1 - y) + 1;
+    if (vi >= 0 && vi < R1) {
+#pragma unroll
+      for (int l = 0; l < Q; ++l) stg[2 * (POP_PAIR(REFL(l)) * R1 + vi) + POP_HALF(REFL(l))] = f[l];
+    }
+  }
+}
+
+// SM100 shared-memory matrix descriptor, K-major, no swizzle (rows of 16 B,
+// 8-row core matrices 128 B apart; version 1), start address saddr
+__device__ __forceinline__ uint64_t stage_desc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)(16 >> 4) << 16) | ((uint64_t)(128 >> 4) << 32) |
+         ((uint64_t)1 << 46);
+}
+
+// one thread: copy staging buffer stg (phase-1 item of local iteration t)
+// into every pair's ring slot t % TP_LT, shifted by 3 - cy rows, then commit
+// the copies to the mbarrier cp_bar
+template <int R1>
+__device__ __forceinline__ void stage_copy(const double* stg, uint32_t tbase, int t, uint32_t cp_bar) {
+  const uint32_t s0 = smem_u32(stg);
+#pragma unroll
+  for (int j = 0; j < NPAIR; ++j) {
+    const uint64_t d = stage_desc(s0 + 16u * (uint32_t)(j * R1 + 3 - TP_CY(j)));
+    const uint32_t dst = tbase + (uint32_t)(TP_COL(j) + 4 * (t % TP_LT(j)));
+    asm volatile("tcgen05.cp.cta_group::1.128x128b [%0], %1;" ::"r"(dst), "l"(d) : "memory");
+  }
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(cp_bar)
+               : "memory");
+}
+
+// phase 2 (lane quarter q = warp % 4, lane = strip row 32 q + lane): the 37
+// populations of state n+1 it pulls, from its own TMEM lane.  Population l
+// comes from the item of iteration t - 4 - cx_l; only the three with cx = -3
+// (labels 34..36) need the newest item t - 1, so their loads follow
+// wait_newest() (the copies of item t - 1 complete) and the other 34 are in
+// flight meanwhile.
+template <class Wait>
+__device__ __forceinline__ void tmem_gather(uint32_t tlane, int t, double (&f)[Q], const Wait& wait_newest) {
+  uint32_t lo[Q], hi[Q];
+  auto ld = [&](int l) {
+    const int j = POP_PAIR(l);
+    const uint32_t a = tlane + (uint32_t)(TP_COL(j) + 4 * ((t - 4 - CX(l)) % TP_LT(j)) + 2 * POP_HALF(l));
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];" : "=r"(lo[l]), "=r"(hi[l]) : "r"(a));
+  };
+#pragma unroll
+  for (int l = 0; l < Q; ++l)
+    if (CX(l) != -3) ld(l);
+  wait_newest();
+#pragma unroll
+  for (int l = 0; l < Q; ++l)
+    if (CX(l) == -3) ld(l);
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int l = 0; l < Q; ++l) {
+    // the registers are written asynchronously: tie every use to the wait
+    asm volatile("" : "+r"(lo[l]), "+r"(hi[l]));
+    f[l] = __hiloint2double((int)hi[l], (int)lo[l]);
+  }
+}
+
 #ifndef LB_TB_HT
 #define LB_TB_HT 104
 #define LB_TB_PF 1
@@ -513,7 +658,7 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
   // phase-1 warps wrote item I; empty[I & 1] — the phase-2 warps finished
   // gathering in iteration I (the slots phase 1 overwrites at I + 1).  A phase
   // can run up to one iteration ahead of the other.
-  constexpr bool DECOUPLE = (LB_TB_DECOUPLE >> (COLL == COLL_REGULARIZED ? 1 : 0)) & 1;
+  constexpr bool DECOUPLE = !LB_TB_TMEM && ((LB_TB_DECOUPLE >> (COLL == COLL_REGULARIZED ? 1 : 0)) & 1);
   static_assert(!DECOUPLE || EARLY, "decoupled phases need the phase-1 warps to issue the loads");
   // NBAR: named barriers F(t) = 3 + (t & 1), "phase 1 wrote iteration t"
   // (phase 1 arrives, phase 2 syncs before its gather of t + 1), and
@@ -527,23 +672,40 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
   // within a sweep, so no generation is left open across sweeps.
   constexpr bool NBAR = !DECOUPLE && ((LB_TB_NBAR >> (COLL == COLL_REGULARIZED ? 1 : 0)) & 1);
   static_assert(!NBAR || EARLY, "named-barrier hand-over needs the phase-1 warps to issue the loads");
+  // TMEM (LB_TB_TMEM): the state-(n+1) ring in tensor memory (see NPAIR);
+  // one CTA-wide barrier per iteration orders the staging, copies and reads
+  constexpr bool TMEM = LB_TB_TMEM;
+  static_assert(!TMEM || (EARLY && !DECOUPLE && !NBAR), "TMEM ring: CTA barrier per iteration, early refill");
+  static_assert(!TMEM || C::NW2 == 4, "TMEM ring: one phase-2 warp per TMEM lane quarter");
   extern __shared__ __align__(128) double sm[];
   double* s0 = sm;
-  double* s1 = sm + C::S0_DBL;
+  double* s1 = sm + C::S0_DBL;  // the ring, or (TMEM) the two staging buffers
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + C::S0_DBL + C::S1_DBL);
+  uint32_t* tbase_smem = reinterpret_cast<uint32_t*>(bars + NB + 6);
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
   const int lx = g.lx, ly = g.ly;
 
+  if (TMEM && warp == 0) {  // the whole 512-column tensor memory (one CTA per SM)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tbase_smem)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
   if (tid == 0) {
     for (int i = 0; i < NB; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bars + i)));
     for (int i = 0; i < 2; ++i) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bars + NB + i)), "r"(32 * C::NW1));
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bars + NB + 2 + i)), "r"(32 * C::NW2));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bars + NB + 4 + i)));  // TMEM copies
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  if (TMEM) asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if (TMEM) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tbase = TMEM ? *tbase_smem : 0u;
+  const uint32_t bar_cp = smem_u32(bars + NB + 4);  // TMEM: copies of phase-1 item k done: bar_cp + 8 (k & 1)
+  // TMEM: this phase-2 warp's lane quarter
+  const uint32_t tlane = tbase + ((uint32_t)(32 * (warp & 3)) << 16);
 
   // Weighted split: a column of a wall strip costs wall_w16 / 16 of an interior
   // one (thermal repopulation and mirror copies on its wall warps), so the CTAs
@@ -673,6 +835,17 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
     for (int t = 0; t < niter; ++t) {
       const uint32_t I = iglob + (uint32_t)t;
       if (!DECOUPLE && !NBAR) __syncthreads();  // every read of iteration t-1 is done: the buffers refilled below are free
+      if (TMEM) {
+        // phase 1 staged item t - 1 and phase 2 finished reading the ring
+        // slots of iteration t - 1 (tcgen05.wait::ld + fence before the
+        // barrier): copy the staging into the ring; a phase-2 lane issues
+        // (that phase waits for phase 1 at the barrier anyway)
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (tid == 32 * C::NW1 && t >= 1 && t - 1 < nload) {
+          const uint32_t k = kglob + (uint32_t)(t - 1);
+          stage_copy<R1>(s1 + (k & 1) * C::STG_DBL, tbase, t - 1, bar_cp + 8 * (k & 1));
+        }
+      }
       if (l2_dist > 0 && t + l2_dist < nload) {
         // L2 prefetch (LSU, not the TMA queue) of the newest column the loads
         // of iteration t + l2_dist touch: rows [ya - 6, ya + HT + 6) of all 37
@@ -728,7 +901,16 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
             phase1_gather<BUFD, RB>(s0, buf, valid ? i : 0, f);
             asm volatile("bar.sync 2, %0;" ::"r"(32 * C::NW1) : "memory");
             if (issuer && t + NB < nload) issue_one(t + NB, my_grp);
-            if (NBAR) {
+            if (TMEM) {
+              if (valid) {
+                phase1_collide<COLL, MON>(f, y, ly, thermal, r, own, acc);
+                // staging buffer kb & 1 was last read by the copies of item kb - 2
+                if (kb >= 2) mbar_wait(bar_cp + 8 * (kb & 1), ((kb - 2) >> 1) & 1);
+                stage_store<R1>(f, s1 + (kb & 1) * C::STG_DBL, i, y, ly);
+                // generic-proxy stores, read next by tcgen05.cp (async proxy)
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+              }
+            } else if (NBAR) {
               if (valid) phase1_collide<COLL, MON>(f, y, ly, thermal, r, own, acc);
               if (t > 0) asm volatile("bar.sync %0, %1;" ::"r"(5 + ((t - 1) & 1)), "r"(C::NT) : "memory");
               if (valid) phase1_store<R1>(f, s1, t, i, y, ly);
@@ -766,6 +948,22 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar_empty + 8 * (I & 1)) : "memory");
         if (valid)
           phase2_update<COLL, MON>(f, B, g, y, xs - 7 + t, thermal, r, y >= own_lo && y < own_hi, acc, !peers);
+      } else if (TMEM) {
+        // phase 2 from the TMEM ring: wait for the copies of the newest item
+        // it pulls (t - 1: the populations with cx = -3), read its own lane
+        if (t >= 7) {
+          const uint32_t k = kglob + (uint32_t)(t - 1);
+          double f[Q];
+          tmem_gather(tlane, t, f, [&] {
+            mbar_wait(bar_cp + 8 * (k & 1), (k >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          });
+          const int i = tid - 32 * C::NW1;
+          const int y = ya + i;
+          if (i < HT && y < ly)
+            phase2_update<COLL, MON>(f, B, g, y, xs - 7 + t, thermal, r, y >= own_lo && y < own_hi, acc, !peers);
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       } else if (t >= 7) {
         // phase 2: state n+2 at column c2 = xs - 7 + t, rows [ya, ya+HT)
         const int i = tid - 32 * C::NW1;
@@ -784,6 +982,12 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
     kglob += (uint32_t)nload;
     iglob += (uint32_t)niter;
     __syncthreads();  // the next sweep refills every ring
+  }
+  if (TMEM) {  // every copy completed (phase 2 waited for the last one of each sweep)
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase));
   }
   if (inpull) {
     // publish this launch (the neighbours may now read our new state and

@@ -59,15 +59,20 @@ for _ in range(3):
         x.step(1)
 for x in r:
     x.sync()
-# two-step kernel at N > 1: staging pull + two-step launches + a one-step
-# remainder (waiting halo pull), monitors on
+# two-step kernel at N > 1: the in-kernel exchange (edge CTAs wait and read
+# the neighbours' buffers by TMA, the last CTA signals) + two-step launches +
+# a one-step remainder (waiting halo pull), monitors on; then the same with
+# the staged exchange (k_tb_wait + k_tb_pull before the kernel, k_signal after)
 for x in r:
     x.monitor(True)
-for _ in range(2):
+for edge in (True, False):
     for x in r:
-        x.step(2)
-for x in r:
-    x.step(1)
-for x in r:
-    x.sync()
+        x.edge_pull(edge)
+    for _ in range(2):
+        for x in r:
+            x.step(2)
+    for x in r:
+        x.step(1)
+    for x in r:
+        x.sync()
 print("sanitize target done", np.isfinite(r[0].peek(0)).all())
