@@ -76,6 +76,14 @@ namespace {
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
+#ifndef LB_TB_WAR_FENCE  // proxy fence between the phase-1 gather and the TMA refill of its buffer
+#define LB_TB_WAR_FENCE 1
+#endif
+// (Measured and rejected: with SKEW in every kernel, phase 2 gathers the
+// populations with cx >= -2 one iteration early, so cx + 4 slots suffice (151
+// instead of 185) and HT = 114 fits (18 strips at ly = 2048 instead of 20):
+// 15.2K MLUPS against 16.4-16.5K — the taller iterations cost more than the
+// 10 % fewer of them save.)
 LB_HD constexpr int L1(int l) { return CX(l) + 5; }
 
 // Literal tables (a constexpr loop evaluated in device code is NOT folded by
@@ -103,7 +111,18 @@ constexpr bool tables_ok() {
 static_assert(tables_ok(), "CXSUM / REFL tables");
 
 // state-(n+1) ring slots of the populations before l
-LB_HD constexpr int SLOTS1_BEFORE(int l) { return CXSUM(l) + 5 * l; }
+LB_HD constexpr int SLOTS1_BEFORE(int l) {
+  return CXSUM(l) + 5 * l;
+}
+constexpr bool slots_ok() {
+  int s = 0;
+  for (int l = 0; l < Q; ++l) {
+    if (SLOTS1_BEFORE(l) != s) return false;
+    s += L1(l);
+  }
+  return SLOTS1_BEFORE(Q) == s;
+}
+static_assert(slots_ok(), "ring slot offsets");
 
 // Column groups.  The labels run cx = +3 .. -3 with cy ascending (App. A), so
 // the populations of one cx are consecutive labels: group g = 3 - cx holds
@@ -899,7 +918,8 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
         const int j = xs + t + l2_dist;  // c1(t + l2_dist) + 3
         if (!peers || j < lx + H) {
           const double* col = Asrc + (int64_t)(peers ? j : wrap_col(j, lx)) * g.cs + (rbase - 6);
-          for (int q = tid; q < Q * 8; q += C::NT)
+          // (SKEW: only the phase-1 warps run this loop)
+          for (int q = tid; q < Q * 8; q += SKEW ? 32 * C::NW1 : C::NT)
             asm volatile("prefetch.global.L2 [%0];" ::"l"(col + (int64_t)(q >> 3) * g.nyp + (q & 7) * 16));
         }
       }
@@ -940,6 +960,11 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
             // with iteration t + NB's windows while the collisions run
             double f[Q];
             phase1_gather<BUFD, RB>(s0, buf, valid ? i : 0, f);
+            // the TMA refill below (async proxy) overwrites what these loads
+            // (generic proxy) read, and a load may still be in flight at the
+            // barrier: order them (write-after-read across proxies).  Without
+            // it, a refill that hits L2 (fast) could land under a pending load.
+            if (LB_TB_WAR_FENCE) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             asm volatile("bar.sync 2, %0;" ::"r"(32 * C::NW1) : "memory");
             if (issuer && t + NB < nload) issue_one(t + NB, my_grp);
             if (TMEM) {

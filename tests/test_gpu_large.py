@@ -108,3 +108,35 @@ def test_two_step_equals_one_step_full_size(lb):
         g.close()
         torch.cuda.empty_cache()
     assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("l2", [1, 2, 3])
+def test_two_step_refill_ordered_after_the_gather(lb, l2):
+    """The phase-1 gather of the two-step kernel reads a state-n buffer with
+    generic-proxy shared-memory loads, then the TMA (async proxy) refills that
+    buffer: without a proxy fence between them a load still in flight at the
+    barrier can read the refill.  A refill that hits L2 is fast enough to land
+    in that window: with the L2 prefetch of the windows on, 4 of 8 such
+    1000-step runs at 1920x2048 differed from the one-step kernel before the
+    fence (profiles/r02_tb_experiments.json, round 2), 0 of 15 after.  Here:
+    600 steps, the current state compared bit for bit on the device."""
+    lx, ly, nsteps = 1920, 2048, 600
+    T0 = oracle.t0()
+    runs = []
+    for tb in (False, True):
+        s = torch.cuda.Stream()
+        g = lb.Lattice(lx, ly, stream=s, temporal=False)
+        if tb:
+            g.temporal(True, l2_prefetch=l2)
+        g.init_macro(*lbgen.rt_macro(lx, ly, T0))
+        g.step(nsteps)
+        g.sync()
+        nyp, y0 = int(g.layout.nyp), int(g.layout.y0)
+        c0 = torch.from_numpy(g.peek_cols(0, 1)[:, 0, :]).cuda()
+        phys = [b.view(-1, 37, nyp)[3:3 + lx, :, y0:y0 + ly] for b in g.bufs]
+        cur = 0 if torch.equal(phys[0][0], c0) else 1
+        assert torch.equal(phys[cur][0], c0)
+        runs.append((g, phys[cur]))
+    assert torch.equal(runs[0][1], runs[1][1])
+    for g, _ in runs:
+        g.close()

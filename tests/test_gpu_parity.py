@@ -737,7 +737,7 @@ def test_two_step_kernel_bit_identical(lb, coll, bc, shape):
         two = sum(v["launches"] for k, v in names.items() if k.startswith("k_step2_tb"))
         if not tb:
             assert two == 0, names
-        elif TB_HT < ly < TB_HT + 6:
+        elif lb.tb_strip_height() < ly < lb.tb_strip_height() + 6:   # (variant builds: their own HT)
             assert two == 0 and names["k_step_fused_reg" if coll == "regularized" else "k_step_fused"][
                 "launches"] == 7, names
         else:
