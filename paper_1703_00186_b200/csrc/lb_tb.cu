@@ -909,12 +909,12 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
       if (l2_dist > 0 && t + l2_dist < nload) {
         // L2 prefetch (LSU, not the TMA queue) of the newest column the loads
         // of iteration t + l2_dist touch: rows [ya - 6, ya + HT + 6) of all 37
-        // planes, 8 lines of 128 B each; N > 1: slab columns only.  (A TMA
-        // L2 prefetch of the whole window — cp.async.bulk.prefetch.tensor, one
-        // instruction — measured 13.5K MLUPS at distance 2 down to 10.3K at
-        // 16 against 15.9K without, and 2 of ~10 such runs differed from the
-        // one-step kernel after 1000 steps, never reproduced with the loads
-        // synchronised per launch; not kept.)
+        // planes, 8 lines of 128 B each; N > 1: slab columns only.  Off by
+        // default (slower at every distance: 14.5K at 1 down to 11.4K at 6,
+        // against 16.5K; a TMA prefetch of the whole window,
+        // cp.async.bulk.prefetch.tensor, was slower still).  With it on the
+        // refills hit L2 — the stress that exposed the gather / refill
+        // write-after-read fixed by LB_TB_WAR_FENCE below.
         const int j = xs + t + l2_dist;  // c1(t + l2_dist) + 3
         if (!peers || j < lx + H) {
           const double* col = Asrc + (int64_t)(peers ? j : wrap_col(j, lx)) * g.cs + (rbase - 6);
