@@ -625,8 +625,8 @@ __device__ __forceinline__ void tmem_gather(uint32_t tlane, int t, double (&f)[Q
 // iteration so that one collides while the other moves data: phase 2 gathers
 // the older 34 populations of its next column at the end of an iteration and
 // only the 3 newest after the barrier, then collides at once, while phase 1
-// gathers; each role runs its own copy of the iteration loop (the same CTA
-// barrier count), so phase 2's populations stay in registers across it.
+// gathers; phase 2's populations stay in registers across the iteration
+// barrier (in the registers phase 1 gathers into).
 #ifndef LB_TB_SKEW
 #define LB_TB_SKEW 1
 #endif
@@ -875,23 +875,11 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
     if (issuer)
       for (int k = 0; k < (EARLY ? NB : PF) && k < nload; ++k) issue_one(k, my_grp);
 
-    if (SKEW && warp >= C::NW1) {
-      // phase 2, offset (SKEW): collide right after the barrier, gather the
-      // next column's older populations after the stores
-      const int i = tid - 32 * C::NW1;
-      const int y = ya + i;
-      const bool valid = i < HT && y < ly;
-      const bool own2 = y >= own_lo && y < own_hi;
-      double f[Q];
-      for (int t = 0; t < niter; ++t) {
-        __syncthreads();  // pairs with the phase-1 loop's barrier of iteration t
-        if (t >= 7) {
-          phase2_gather_part<R1, true>(s1, t, valid ? i : 0, f);
-          if (valid) phase2_update<COLL, MON>(f, B, g, y, xs - 7 + t, thermal, r, own2, acc, !peers);
-        }
-        if (t + 1 >= 7 && t + 1 < niter) phase2_gather_part<R1, false>(s1, t + 1, valid ? i : 0, f);
-      }
-    } else
+    // SKEW: phase 2's next-column populations are carried across the
+    // iteration barrier in fk; phase 1 gathers into the same registers (it
+    // overwrites all of them before any use), so the carried values add no
+    // register pressure to its path
+    double fk[Q];
     for (int t = 0; t < niter; ++t) {
       const uint32_t I = iglob + (uint32_t)t;
       if (!DECOUPLE && !NBAR) __syncthreads();  // every read of iteration t-1 is done: the buffers refilled below are free
@@ -918,8 +906,7 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
         const int j = xs + t + l2_dist;  // c1(t + l2_dist) + 3
         if (!peers || j < lx + H) {
           const double* col = Asrc + (int64_t)(peers ? j : wrap_col(j, lx)) * g.cs + (rbase - 6);
-          // (SKEW: only the phase-1 warps run this loop)
-          for (int q = tid; q < Q * 8; q += SKEW ? 32 * C::NW1 : C::NT)
+          for (int q = tid; q < Q * 8; q += C::NT)
             asm volatile("prefetch.global.L2 [%0];" ::"l"(col + (int64_t)(q >> 3) * g.nyp + (q & 7) * 16));
         }
       }
@@ -958,7 +945,8 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
           if (EARLY) {
             // gather, then (all phase-1 warps done reading) refill the buffer
             // with iteration t + NB's windows while the collisions run
-            double f[Q];
+            double fl[Q];
+            double(&f)[Q] = SKEW ? fk : fl;
             phase1_gather<BUFD, RB>(s0, buf, valid ? i : 0, f);
             // the TMA refill below (async proxy) overwrites what these loads
             // (generic proxy) read, and a load may still be in flight at the
@@ -1014,6 +1002,19 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar_empty + 8 * (I & 1)) : "memory");
         if (valid)
           phase2_update<COLL, MON>(f, B, g, y, xs - 7 + t, thermal, r, y >= own_lo && y < own_hi, acc, !peers);
+      } else if (SKEW) {
+        // phase 2, offset against phase 1: collide right after the barrier
+        // (only the 3 newest populations still to load), then gather the
+        // next column's older populations after the stores
+        const int i = tid - 32 * C::NW1;
+        const int y = ya + i;
+        const bool valid = i < HT && y < ly;
+        if (t >= 7) {
+          phase2_gather_part<R1, true>(s1, t, valid ? i : 0, fk);
+          if (valid)
+            phase2_update<COLL, MON>(fk, B, g, y, xs - 7 + t, thermal, r, y >= own_lo && y < own_hi, acc, !peers);
+        }
+        if (t + 1 >= 7 && t + 1 < niter) phase2_gather_part<R1, false>(s1, t + 1, valid ? i : 0, fk);
       } else if (TMEM) {
         // phase 2 from the TMEM ring: wait for the copies of the newest item
         // it pulls (t - 1: the populations with cx = -3), read its own lane

@@ -2,7 +2,7 @@
 # Round 2 evidence job: bench (both arms), ncu launch list of the bench command, ncu metrics of the hot
 # kernels (-> profiles/ncu_summary.json via tools/ncu_summarize.py), ncu --set full of the two-step kernel,
 # sanitizers over every kernel and transport.
-O=gpurun_out/r02w
+O=${O:-gpurun_out/r02w}
 mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O/smi.txt
 timeout 900 python bench.py > $O/bench.json 2> $O/bench.err; head -c 600 $O/bench.json; echo
