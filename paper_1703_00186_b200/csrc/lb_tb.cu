@@ -62,6 +62,9 @@
 #ifndef LB_TB_STCS
 #define LB_TB_STCS 0
 #endif
+#ifndef LB_TB_ALIGN  // time-aligned work split (see the kernel)
+#define LB_TB_ALIGN 0
+#endif
 #ifndef LB_TB_CLOCK  // variant builds only: per-CTA start/end times (tools/tb_clock.py)
 #define LB_TB_CLOCK 0
 #endif
@@ -778,7 +781,59 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
   int64_t wtot = 0;
   for (int s = 0; s < nstrips; ++s) wtot += (int64_t)(lx + (s > 0 ? TB_LEAD : 0)) * strip_w(s);
   int64_t u = unit_at(wtot * blockIdx.x / gridDim.x);
-  const int64_t u_end = unit_at(wtot * (blockIdx.x + 1) / gridDim.x);
+  int64_t u_end = unit_at(wtot * (blockIdx.x + 1) / gridDim.x);
+  // LB_TB_ALIGN: time-aligned split.  R = grid / nstrips CTAs per strip sweep
+  // the same column ranges [r c_s, (r + 1) c_s) of every strip at the same
+  // time (main region [0, R c_s), c_s shorter on the heavier wall strips), so
+  // the 20 CTAs of one range write (and read) whole population columns
+  // together; the E = grid - R nstrips remaining CTAs share the columns
+  // [R c_s, lx) of every strip (tail region) by the weighted split above.
+  const int R_al = LB_TB_ALIGN && nstrips > 1 ? (int)gridDim.x / nstrips : 0;
+  const int E_al = (int)gridDim.x - R_al * nstrips;
+  const bool aligned = R_al >= 1 && E_al >= 1;
+  const bool tail = aligned && (int)blockIdx.x >= R_al * nstrips;
+  int64_t t16 = 0;
+  for (int s = 0; s < nstrips; ++s) t16 += (int64_t)lx * strip_w(s);
+  t16 = (t16 + (int64_t)16 * TB_LEAD * (gridDim.x + nstrips)) / gridDim.x;  // weighted work per CTA
+  auto main_cols = [&](int s) -> int {
+    const int c = (int)std::max<int64_t>(1, t16 / strip_w(s) - TB_LEAD);
+    return (int64_t)c * R_al >= lx ? (lx + R_al - 1) / R_al : c;
+  };
+  auto tail_lo = [&](int s) -> int { return tail ? std::min(lx, R_al * main_cols(s)) : 0; };
+  if (aligned && !tail) {
+    const int s = (int)blockIdx.x % nstrips, r = (int)blockIdx.x / nstrips, c = main_cols(s);
+    u = (int64_t)s * lx + std::min(lx, r * c);
+    u_end = (int64_t)s * lx + std::min(lx, (r + 1) * c);
+  } else if (tail) {
+    // the tail sequence: strip s contributes its columns [tail_lo(s), lx)
+    auto tail_at = [&](int64_t T) -> int64_t {
+      int64_t acc = 0;
+      bool first = true;
+      for (int s = 0; s < nstrips; ++s) {
+        const int lo = tail_lo(s), w = strip_w(s);
+        if (lo >= lx) continue;
+        if (!first) {
+          acc += (int64_t)TB_LEAD * w;
+          if (T < acc) return (int64_t)s * lx + lo;
+        }
+        first = false;
+        const int64_t sw = (int64_t)(lx - lo) * w;
+        if (T < acc + sw) return (int64_t)s * lx + lo + (T - acc + w - 1) / w;
+        acc += sw;
+      }
+      return (int64_t)nstrips * lx;
+    };
+    int64_t wt = 0;
+    bool first = true;
+    for (int s = 0; s < nstrips; ++s)
+      if (tail_lo(s) < lx) {
+        wt += (int64_t)(lx - tail_lo(s) + (first ? 0 : TB_LEAD)) * strip_w(s);
+        first = false;
+      }
+    const int e = (int)blockIdx.x - R_al * nstrips;
+    u = tail_at(wt * e / E_al);
+    u_end = tail_at(wt * (e + 1) / E_al);
+  }
 #if LB_TB_CLOCK
   unsigned long long clk0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(clk0));
@@ -792,6 +847,10 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
   while (u < u_end) {
     const int strip = (int)(u / lx);
     const int x0 = (int)(u % lx);
+    if (x0 < tail_lo(strip)) {  // (tail CTAs) the main region of this strip is not theirs
+      u = (int64_t)strip * lx + tail_lo(strip);
+      continue;
+    }
     const int x1 = (int)std::min<int64_t>(lx, x0 + (u_end - u));
     u += x1 - x0;
     const int xs = H + x0, W = x1 - x0;  // output columns [xs, xs + W)
