@@ -57,7 +57,7 @@ constexpr int BUFD = goff(NG);  // doubles per state-n buffer
 constexpr int MAXBUF = HT > 200 ? 2 : 6;
 
 struct Maps {
-  CUtensorMap m[3];
+  CUtensorMap m[3], m2[3];  // 3-D {rows, 37, columns} and 2-D {rows, 37 columns} maps
 };
 
 __device__ __forceinline__ uint32_t s32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(NCONS + 32, 1)
       }
       asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(s32(full + b)) : "memory");
     };
-    if (load >= 2 && warp < NCONS / 32) {
+    if ((load == 2 || load == 3) && warp < NCONS / 32) {
       asm volatile("bar.sync 1, %0;" ::"r"(NCONS) : "memory");  // the previous sweep's reads are done
       for (int t = 0; t < nbuf && t < nit; ++t) ldgsts(t);
     }
@@ -179,11 +179,18 @@ __global__ void __launch_bounds__(NCONS + 32, 1)
           }
           int col = xs - 3 + t - (3 - lane) - H;  // group g = lane has cx = 3 - g
           col = ((col % lx) + lx) % lx + H;
-          asm volatile(
-              "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
-              "%4}], [%5];" ::"r"(s32(sm + b * BUFD + goff(lane))),
-              "l"(&mp.m[gcls(lane)]), "r"(Y0 + ya - 6), "r"(gfirst(lane)), "r"(col), "r"(s32(full + b))
-              : "memory");
+          if (load == 4)  // the same box through a 2-D map: planes col * 37 + l have the uniform stride nyp
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+                "[%4];" ::"r"(s32(sm + b * BUFD + goff(lane))),
+                "l"(&mp.m2[gcls(lane)]), "r"(Y0 + ya - 6), "r"(col * Q + gfirst(lane)), "r"(s32(full + b))
+                : "memory");
+          else
+            asm volatile(
+                "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+                "%4}], [%5];" ::"r"(s32(sm + b * BUFD + goff(lane))),
+                "l"(&mp.m[gcls(lane)]), "r"(Y0 + ya - 6), "r"(gfirst(lane)), "r"(col), "r"(s32(full + b))
+                : "memory");
         }
     } else {
       for (int t = 0; t < nit; ++t) {
@@ -200,7 +207,7 @@ __global__ void __launch_bounds__(NCONS + 32, 1)
 #pragma unroll
               for (int j = 0; j < gn(g); ++j) p[(int64_t)(gfirst(g) + j) * nyp] = buf[goff(g) + j * RB + 6 + tid];
           }
-          if (load >= 2) {
+          if (load == 2 || load == 3) {
             asm volatile("bar.sync 1, %0;" ::"r"(NCONS) : "memory");
             if (load == 3) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s32(empty + b)) : "memory");
             if (t + nbuf < nit) ldgsts(t + nbuf);
@@ -224,7 +231,7 @@ __global__ void __launch_bounds__(NCONS + 32, 1)
             if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s32(empty + b)) : "memory");
           }
         } else {  // store == 2: reads only
-          if (load >= 2) {
+          if (load == 2 || load == 3) {
             asm volatile("bar.sync 1, %0;" ::"r"(NCONS) : "memory");
             if (load == 3) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s32(empty + b)) : "memory");
             if (t + nbuf < nit) ldgsts(t + nbuf);
@@ -261,6 +268,13 @@ int main(int argc, char** argv) {
     CUresult r = cuTensorMapEncodeTiled(&mp.m[c], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, A, dims, str, box, es,
                                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                                         CU_TENSOR_MAP_L2_PROMOTION_L2_64B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    cuuint64_t dims2[2] = {(cuuint64_t)nyp, (cuuint64_t)Q * cols};
+    cuuint64_t str2[1] = {(cuuint64_t)nyp * 8};
+    cuuint32_t box2[2] = {RB, (cuuint32_t)(3 + 2 * c)}, es2[2] = {1, 1};
+    if (r == CUDA_SUCCESS)
+      r = cuTensorMapEncodeTiled(&mp.m2[c], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, A, dims2, str2, box2, es2,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_64B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
       fprintf(stderr, "tensor map %d: %d\n", c, (int)r);
       return 1;
@@ -315,18 +329,18 @@ int main(int argc, char** argv) {
   const double ms_copy = timeit([&] { k_copy<<<nsm * 8, 512>>>((const double2*)A, (double2*)B, n / 2); });
   printf("{\"probe\": \"double2 copy\", \"ms\": %.4f, \"gbs\": %.1f}\n", ms_copy, 2.0 * n * 8 / ms_copy * 1e-6);
   const char* sname[4] = {"stg", "bulk", "loads only", "stores only"};
-  const char* lname[4] = {"tma group boxes", "1-D bulk per population", "ldgsts 16 B", "tma + ldgsts"};
+  const char* lname[5] = {"tma group boxes", "1-D bulk per population", "ldgsts 16 B", "tma + ldgsts", "tma group boxes, 2-D map"};
   const int tma_mask = getenv("PROBE_TMA_MASK") ? atoi(getenv("PROBE_TMA_MASK")) : 0x6b;
   const int only_load = getenv("PROBE_LOAD") ? atoi(getenv("PROBE_LOAD")) : -1;
   const int nb_list[3] = {1, 2, 4};
-  for (int load = 0; load < 4; ++load)
+  for (int load = 0; load < 5; ++load)
     for (int aligned = 0; aligned < 2; ++aligned)
       for (int store = 0; store < 4; ++store)
         for (int nbuf : nb_list) {
           if (nbuf > MAXBUF || (only_load >= 0 && load != only_load)) continue;
           if (store == 3 && (nbuf != 2 || load)) continue;
-          if (store == 1 && (nbuf == 1 || load)) continue;
-          if (load && aligned) continue;
+          if (store == 1 && (nbuf == 1 || (load && load != 4))) continue;
+          if (load && load != 4 && aligned) continue;
           const int grid = aligned ? nsm / ns * ns : nsm;
           double ld_bytes, st_bytes;
           req(grid, aligned, ld_bytes, st_bytes);
