@@ -57,7 +57,7 @@ constexpr int BUFD = goff(NG);  // doubles per state-n buffer
 constexpr int MAXBUF = HT > 200 ? 2 : 6;
 
 struct Maps {
-  CUtensorMap m[3], m2[3];  // 3-D {rows, 37, columns} and 2-D {rows, 37 columns} maps
+  CUtensorMap m[12], m2[3];  // m[3 (depth - 1) + class]: boxes of depth 1-4 columns  // 3-D {rows, 37, columns} and 2-D {rows, 37 columns} maps
 };
 
 __device__ __forceinline__ uint32_t s32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -245,6 +245,85 @@ __global__ void __launch_bounds__(NCONS + 32, 1)
   if (store == 1 && warp == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// Boxes of DEPTH consecutive columns: one TMA box per group loads the windows of
+// DEPTH iterations at once ({116 rows, n populations, DEPTH columns}), DEPTH
+// output columns stored per iteration — tests whether the TMA cost is per box
+// (fewer, bigger boxes help) or per row (they do not).
+__host__ __device__ constexpr int goffd(int g, int depth) {
+  int o = 0;
+  for (int h = 0; h < g; ++h) o += (depth * gn(h) * RB + 15) / 16 * 16;
+  return o;
+}
+template <int DEPTH>
+__global__ void __launch_bounds__(NCONS + 32, 1)
+    k_probe_deep(const __grid_constant__ Maps mp, double* __restrict__ B, int lx, int ly, int nyp, int ns, int nbuf,
+                 int store) {
+  extern __shared__ __align__(128) double sm[];
+  constexpr int BD = goffd(NG, DEPTH);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + MAXBUF * BUFD);
+  uint64_t* empty = full + MAXBUF;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t cs = (int64_t)Q * nyp;
+  if (tid == 0) {
+    for (int i = 0; i < nbuf; ++i) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s32(full + i)));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s32(empty + i)), "r"(NCONS));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t U = (int64_t)ns * lx;
+  int64_t u = U * blockIdx.x / gridDim.x;
+  const int64_t ue = U * (blockIdx.x + 1) / gridDim.x;
+  uint32_t k = 0;
+  while (u < ue) {
+    const int s = (int)(u / lx), x0 = (int)(u % lx);
+    const int x1 = (int)std::min<int64_t>(lx, x0 + (ue - u));
+    u += x1 - x0;
+    const int ya = strip_ya(s, ns, ly), xs = H + x0, W = x1 - x0;
+    const int nit = (W + 6 + DEPTH - 1) / DEPTH;  // iterations of DEPTH load columns
+    if (warp == NCONS / 32) {
+      if (lane < NG)
+        for (int t = 0; t < nit; ++t) {
+          const uint32_t kb = k + t, b = kb % nbuf;
+          if (kb >= (uint32_t)nbuf) mbar_wait(s32(empty + b), ((kb / nbuf) - 1) & 1);
+          if (lane == 0)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s32(full + b)),
+                         "r"((uint32_t)(DEPTH * Q * RB * 8)));
+          int col = xs - 3 + DEPTH * t - (3 - lane);  // first of DEPTH columns (no wrap: interior only)
+          if (col < H) col += lx;
+          if (col + DEPTH > lx + H) col = lx + H - DEPTH;  // (clamped at the right edge: bytes, not values, matter)
+          asm volatile(
+              "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+              "%4}], [%5];" ::"r"(s32(sm + b * BD + goffd(lane, DEPTH))),
+              "l"(&mp.m[3 * (DEPTH - 1) + gcls(lane)]), "r"(Y0 + ya - 6), "r"(gfirst(lane)), "r"(col),
+              "r"(s32(full + b))
+              : "memory");
+        }
+    } else {
+      for (int t = 0; t < nit; ++t) {
+        const uint32_t kb = k + t, b = kb % nbuf;
+        mbar_wait(s32(full + b), (kb / nbuf) & 1);
+        const double* buf = sm + b * BD;
+        if (store == 0 && tid < HT && ya + tid < ly)
+#pragma unroll
+          for (int j = 0; j < DEPTH; ++j) {
+            const int c2 = xs - 6 + DEPTH * t + j;
+            if (c2 < xs || c2 >= xs + W) continue;
+            double* p = B + (int64_t)c2 * cs + Y0 + ya + tid;
+#pragma unroll
+            for (int g = 0; g < NG; ++g)
+#pragma unroll
+              for (int i = 0; i < gn(g); ++i)
+                p[(int64_t)(gfirst(g) + i) * nyp] = buf[goffd(g, DEPTH) + (j * gn(g) + i) * RB + 6 + tid];
+          }
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s32(empty + b)) : "memory");
+      }
+    }
+    k += nit;
+  }
+}
+
 __global__ void k_copy(const double2* __restrict__ a, double2* __restrict__ b, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     b[i] = a[i];
@@ -264,6 +343,13 @@ int main(int argc, char** argv) {
   for (int c = 0; c < 3; ++c) {
     cuuint64_t dims[3] = {(cuuint64_t)nyp, (cuuint64_t)Q, (cuuint64_t)cols};
     cuuint64_t str[2] = {(cuuint64_t)nyp * 8, (cuuint64_t)Q * nyp * 8};
+    for (int d = 2; d <= 4; ++d) {
+      cuuint32_t boxd[3] = {RB, (cuuint32_t)(3 + 2 * c), (cuuint32_t)d}, esd[3] = {1, 1, 1};
+      if (cuTensorMapEncodeTiled(&mp.m[3 * (d - 1) + c], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, A, dims, str, boxd, esd,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_64B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return 1;
+    }
     cuuint32_t box[3] = {RB, (cuuint32_t)(3 + 2 * c), 1}, es[3] = {1, 1, 1};
     CUresult r = cuTensorMapEncodeTiled(&mp.m[c], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, A, dims, str, box, es,
                                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -355,5 +441,26 @@ int main(int argc, char** argv) {
                  nbuf * Q * RB * 8 / 1024.0, ms, bytes / ms * 1e-6, ld_bytes * 1e-9, st_bytes * 1e-9,
                  2 * sites / ms * 1e-3);
         }
+  if (getenv("PROBE_DEEP")) {
+    auto run_deep = [&](auto kern, int depth) {
+      CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      const int maxb = (int)((MAXBUF * BUFD) / goffd(NG, depth));
+      for (int store = 0; store < 3; store += 2)
+        for (int nbuf = 1; nbuf <= std::min(maxb, 4); ++nbuf) {
+          double ld_bytes, st_bytes;
+          req(nsm, 0, ld_bytes, st_bytes);
+          const double ms = timeit([&] { kern<<<nsm, NCONS + 32, smem>>>(mp, B, lx, ly, nyp, ns, nbuf, store); });
+          const double bytes = ld_bytes + (store == 0 ? st_bytes : 0);
+          printf("{\"probe\": \"deep boxes\", \"depth\": %d, \"store\": \"%s\", \"nbuf\": %d, \"kb_in_flight_max\": %.1f, "
+                 "\"ms\": %.4f, \"requested_gbs\": %.1f, \"mlups_if_kernel\": %.0f}\n",
+                 depth, store == 0 ? "stg" : "loads only", nbuf, nbuf * depth * Q * RB * 8 / 1024.0, ms,
+                 bytes / ms * 1e-6, 2 * sites / ms * 1e-3);
+        }
+    };
+    run_deep(k_probe_deep<1>, 1);
+    run_deep(k_probe_deep<2>, 2);
+    run_deep(k_probe_deep<4>, 4);
+    return 0;
+  }
   return 0;
 }
