@@ -62,8 +62,16 @@
 #ifndef LB_TB_STCS
 #define LB_TB_STCS 0
 #endif
-#ifndef LB_TB_ALIGN  // time-aligned work split (see the kernel)
-#define LB_TB_ALIGN 0
+// bit 0: BGK, bit 1: regularised — time-aligned work split (see the kernel;
+// default BGK: +0.7 % in two A/B runs on one box; regularised: -4.8 %)
+#ifndef LB_TB_ALIGN
+#define LB_TB_ALIGN 1
+#endif
+// clusters of 2 CTAs sweeping adjacent strips in lockstep (see the kernel;
+// variant builds only: -3 %, the per-iteration cluster barrier costs more than
+// the 208-row store runs gain)
+#ifndef LB_TB_PAIR
+#define LB_TB_PAIR 0
 #endif
 #ifndef LB_TB_CLOCK  // variant builds only: per-CTA start/end times (tools/tb_clock.py)
 #define LB_TB_CLOCK 0
@@ -764,10 +772,19 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
   // start absorbs (unit_at maps T inside it to the strip start).
   constexpr int TB_LEAD = LB_TB_LEAD;
   auto strip_w = [&](int s) { return (nstrips > 1 && (s == 0 || s == nstrips - 1)) ? wall_w16 : 16; };
+  // LB_TB_PAIR (variant, launched as clusters of 2 CTAs): the two CTAs of a
+  // cluster sweep two vertically adjacent strips (a "virtual strip") over the
+  // same columns in lockstep (a cluster barrier per iteration), so their
+  // state-n+2 stores form 208-row runs; the split below then works on virtual
+  // strips (pairs, weighted by the heavier strip) and cluster indices.
+  const bool paired = LB_TB_PAIR && nstrips % 2 == 0 && gridDim.x % 2 == 0;
+  const int CL = paired ? 2 : 1;
+  const int nv = nstrips / CL, ng = (int)gridDim.x / CL, gid = (int)blockIdx.x / CL, rank = (int)blockIdx.x % CL;
+  auto vw = [&](int v) { return CL == 1 ? strip_w(v) : std::max(strip_w(2 * v), strip_w(2 * v + 1)); };
   auto unit_at = [&](int64_t T) -> int64_t {
     int64_t acc = 0;
-    for (int s = 0; s < nstrips; ++s) {
-      const int w = strip_w(s);
+    for (int s = 0; s < nv; ++s) {
+      const int w = vw(s);
       if (s > 0) {
         acc += (int64_t)TB_LEAD * w;
         if (T < acc) return (int64_t)s * lx;
@@ -776,41 +793,44 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
       if (T < acc + sw) return (int64_t)s * lx + (T - acc + w - 1) / w;
       acc += sw;
     }
-    return (int64_t)nstrips * lx;
+    return (int64_t)nv * lx;
   };
   int64_t wtot = 0;
-  for (int s = 0; s < nstrips; ++s) wtot += (int64_t)(lx + (s > 0 ? TB_LEAD : 0)) * strip_w(s);
-  int64_t u = unit_at(wtot * blockIdx.x / gridDim.x);
-  int64_t u_end = unit_at(wtot * (blockIdx.x + 1) / gridDim.x);
-  // LB_TB_ALIGN: time-aligned split.  R = grid / nstrips CTAs per strip sweep
-  // the same column ranges [r c_s, (r + 1) c_s) of every strip at the same
-  // time (main region [0, R c_s), c_s shorter on the heavier wall strips), so
-  // the 20 CTAs of one range write (and read) whole population columns
-  // together; the E = grid - R nstrips remaining CTAs share the columns
-  // [R c_s, lx) of every strip (tail region) by the weighted split above.
-  const int R_al = LB_TB_ALIGN && nstrips > 1 ? (int)gridDim.x / nstrips : 0;
-  const int E_al = (int)gridDim.x - R_al * nstrips;
+  for (int s = 0; s < nv; ++s) wtot += (int64_t)(lx + (s > 0 ? TB_LEAD : 0)) * vw(s);
+  // units u: (virtual strip, column) = v lx + x
+  int64_t u = unit_at(wtot * gid / ng);
+  int64_t u_end = unit_at(wtot * (gid + 1) / ng);
+  // LB_TB_ALIGN / LB_TB_PAIR: time-aligned split.  R = ng / nv work units
+  // (CTAs or clusters) per virtual strip sweep the same column ranges
+  // [r c_v, (r + 1) c_v) of every virtual strip at the same time (main region
+  // [0, R c_v), c_v shorter on the heavier wall strips), so the units of one
+  // range write (and read) whole population columns together; the
+  // E = ng - R nv remaining units share the columns [R c_v, lx) of every
+  // virtual strip (tail region) by the weighted split above.
+  constexpr bool ALIGN = (LB_TB_ALIGN >> (COLL == COLL_REGULARIZED ? 1 : 0)) & 1;
+  const int R_al = (ALIGN || paired) && nv > 1 ? ng / nv : 0;
+  const int E_al = ng - R_al * nv;
   const bool aligned = R_al >= 1 && E_al >= 1;
-  const bool tail = aligned && (int)blockIdx.x >= R_al * nstrips;
+  const bool tail = aligned && gid >= R_al * nv;
   int64_t t16 = 0;
-  for (int s = 0; s < nstrips; ++s) t16 += (int64_t)lx * strip_w(s);
-  t16 = (t16 + (int64_t)16 * TB_LEAD * (gridDim.x + nstrips)) / gridDim.x;  // weighted work per CTA
+  for (int s = 0; s < nv; ++s) t16 += (int64_t)lx * vw(s);
+  t16 = (t16 + (int64_t)16 * TB_LEAD * (ng + nv)) / ng;  // weighted work per unit
   auto main_cols = [&](int s) -> int {
-    const int c = (int)std::max<int64_t>(1, t16 / strip_w(s) - TB_LEAD);
+    const int c = (int)std::max<int64_t>(1, t16 / vw(s) - TB_LEAD);
     return (int64_t)c * R_al >= lx ? (lx + R_al - 1) / R_al : c;
   };
   auto tail_lo = [&](int s) -> int { return tail ? std::min(lx, R_al * main_cols(s)) : 0; };
   if (aligned && !tail) {
-    const int s = (int)blockIdx.x % nstrips, r = (int)blockIdx.x / nstrips, c = main_cols(s);
+    const int s = gid % nv, r = gid / nv, c = main_cols(s);
     u = (int64_t)s * lx + std::min(lx, r * c);
     u_end = (int64_t)s * lx + std::min(lx, (r + 1) * c);
   } else if (tail) {
-    // the tail sequence: strip s contributes its columns [tail_lo(s), lx)
+    // the tail sequence: virtual strip s contributes its columns [tail_lo(s), lx)
     auto tail_at = [&](int64_t T) -> int64_t {
       int64_t acc = 0;
       bool first = true;
-      for (int s = 0; s < nstrips; ++s) {
-        const int lo = tail_lo(s), w = strip_w(s);
+      for (int s = 0; s < nv; ++s) {
+        const int lo = tail_lo(s), w = vw(s);
         if (lo >= lx) continue;
         if (!first) {
           acc += (int64_t)TB_LEAD * w;
@@ -821,16 +841,16 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
         if (T < acc + sw) return (int64_t)s * lx + lo + (T - acc + w - 1) / w;
         acc += sw;
       }
-      return (int64_t)nstrips * lx;
+      return (int64_t)nv * lx;
     };
     int64_t wt = 0;
     bool first = true;
-    for (int s = 0; s < nstrips; ++s)
+    for (int s = 0; s < nv; ++s)
       if (tail_lo(s) < lx) {
-        wt += (int64_t)(lx - tail_lo(s) + (first ? 0 : TB_LEAD)) * strip_w(s);
+        wt += (int64_t)(lx - tail_lo(s) + (first ? 0 : TB_LEAD)) * vw(s);
         first = false;
       }
-    const int e = (int)blockIdx.x - R_al * nstrips;
+    const int e = gid - R_al * nv;
     u = tail_at(wt * e / E_al);
     u_end = tail_at(wt * (e + 1) / E_al);
   }
@@ -843,14 +863,16 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
   uint32_t iglob = 0;  // DECOUPLE: iterations of this CTA over all its sweeps (ring items)
   const uint32_t bar_full = smem_u32(bars + NB), bar_empty = smem_u32(bars + NB + 2);
   double acc[5] = {0.0, 0.0, 0.0, 0.0, INFINITY};  // MON: this thread's state (n+1 or n+2)
+  bool cl_armed = false;  // PAIR: a cluster-barrier arrival is pending
 
   while (u < u_end) {
-    const int strip = (int)(u / lx);
+    const int vstrip = (int)(u / lx);
     const int x0 = (int)(u % lx);
-    if (x0 < tail_lo(strip)) {  // (tail CTAs) the main region of this strip is not theirs
-      u = (int64_t)strip * lx + tail_lo(strip);
+    if (x0 < tail_lo(vstrip)) {  // (tail units) the main region of this strip is not theirs
+      u = (int64_t)vstrip * lx + tail_lo(vstrip);
       continue;
     }
+    const int strip = vstrip * CL + rank;
     const int x1 = (int)std::min<int64_t>(lx, x0 + (u_end - u));
     u += x1 - x0;
     const int xs = H + x0, W = x1 - x0;  // output columns [xs, xs + W)
@@ -942,6 +964,13 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
     for (int t = 0; t < niter; ++t) {
       const uint32_t I = iglob + (uint32_t)t;
       if (!DECOUPLE && !NBAR) __syncthreads();  // every read of iteration t-1 is done: the buffers refilled below are free
+      if (LB_TB_PAIR && paired) {
+        // lockstep with the other CTA of the cluster: wait for its arrival of
+        // the previous iteration (latency hidden behind one iteration), arrive
+        if (cl_armed) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+        asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+        cl_armed = true;
+      }
       if (TMEM) {
         // phase 1 staged item t - 1 and phase 2 finished reading the ring
         // slots of iteration t - 1 (tcgen05.wait::ld + fence before the
@@ -1109,6 +1138,7 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
     iglob += (uint32_t)niter;
     __syncthreads();  // the next sweep refills every ring
   }
+  if (LB_TB_PAIR && cl_armed) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
   if (TMEM) {  // every copy completed (phase 2 waited for the last one of each sweep)
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
@@ -1224,6 +1254,25 @@ cudaError_t launch_tb(const Geo& g, const TbMaps* t, int src_buf, double* B, con
     km.stR[c] = !peers ? t->load[src_buf][c] : inpull ? t->nb[1][src_buf][c] : t->st[1][c];
   }
   const TbPeer pp = inpull ? *pull : TbPeer{};
+#if LB_TB_PAIR
+  if (tb_grid(g, grid) >= 2) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(tb_grid(g, grid) & ~1));
+    cfg.blockDim = dim3(Cfg::NT);
+    cfg.dynamicSmemBytes = Cfg::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const double* asrc = t->bufs[src_buf];
+    const int nstr = (g.ly + TB_HT - 1) / TB_HT, ip = inpull ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, km, B, g, r, nstr, l2_dist, thermal, wall_w16, mon, peers, asrc, pp, ip);
+  }
+#endif
   kern<<<tb_grid(g, grid), Cfg::NT, Cfg::SMEM, s>>>(km, B, g, r, (g.ly + TB_HT - 1) / TB_HT, l2_dist, thermal,
                                                     wall_w16, mon, peers, t->bufs[src_buf], pp,
                                                     inpull ? 1 : 0);
