@@ -150,6 +150,7 @@ struct lb_ctx {
   int tb_l2 = 0;                // LB_OPT_TB_L2_PREFETCH: L2 prefetch distance in columns
   int tb_promo = 64;            // LB_OPT_TB_L2_PROMOTION: L2 promotion of its TMA loads (bytes)
   int tb_wall_w16 = 0;          // LB_OPT_TB_WALL_WEIGHT: wall-strip column cost x16 (work split; 0 = per collision)
+  int tb_tail_w16 = 0;          // LB_OPT_TB_TAIL_WEIGHT: tail-region column cost x16 (aligned split; 0 = default)
   int tb_edge_pull = 1;         // LB_OPT_TB_EDGE_PULL: N > 1 two-step exchange inside the kernel (1) or k_tb_pull first (0)
   double* d_stage = nullptr;    // N > 1 two-step: the neighbours' 6 edge columns (2 x 6 x cs doubles)
   unsigned int* d_ctas = nullptr;  // N > 1 two-step, in-kernel exchange: finished-CTA count (kept zero)
@@ -857,9 +858,23 @@ static bool tb_usable(const lb_ctx* c) {
 // two-step kernel's work split: measured per-CTA times (tools/tb_clock.py,
 // 1920x2048) give 1.17 (BGK) and 1.25 (regularised) per iteration, and a
 // sweep of the BGK weight 17..21 peaks at 19.
+// BGK uses the time-aligned split (LB_OPT_TB_TAIL_WEIGHT != 1), where a
+// wall-strip column costs 1.28x an interior one (per-CTA clocks: 1.92 vs 1.50
+// us per iteration) and a weight sweep (tools/gpu_job_r02_wt.sh) peaks at
+// wall 21 / tail 17 (x1/16); with the contiguous split 19 (BGK) and 20
+// (regularised) balance best.
+static bool tb_aligned(const lb_ctx* c) {
+  return c->p.collision != LB_COLLIDE_REGULARIZED && c->tb_tail_w16 != 1;
+}
 static int tb_wall_weight(const lb_ctx* c) {
   if (c->tb_wall_w16 > 0) return c->tb_wall_w16;
-  return c->p.collision == LB_COLLIDE_REGULARIZED ? 20 : 19;
+  return c->p.collision == LB_COLLIDE_REGULARIZED ? 20 : tb_aligned(c) ? 21 : 19;
+}
+// The kernel's split parameter: wall weight | tail weight << 16 (both x16;
+// tail 0: the contiguous split).
+static int tb_split_weights(const lb_ctx* c) {
+  const int tail = !tb_aligned(c) ? 0 : c->tb_tail_w16 >= 16 ? c->tb_tail_w16 : 17;
+  return tb_wall_weight(c) | (tail << 16);
 }
 
 static int step_tb(lb_ctx* c) {
@@ -897,7 +912,7 @@ static int step_tb(lb_ctx* c) {
   }
   TRY(launch(c, c->p.collision ? "k_step2_tb_reg" : "k_step2_tb", c->s, 2 * c->L.sites, [&] {
     return lbk::launch_step2_tb(c->g, c->tb, c->par, c->B, c->p.bc_y, c->p.collision, c->relax, grid, c->tb_l2,
-                                tb_wall_weight(c), mon, peers ? 1 : 0, inpull ? &pull : nullptr, c->s);
+                                tb_split_weights(c), mon, peers ? 1 : 0, inpull ? &pull : nullptr, c->s);
   }));
   if (peers) {  // publish: this launch is complete (the neighbours may now read our new state)
     c->peer_step += 1;
@@ -1189,6 +1204,11 @@ int lb_set_option(lb_ctx* c, int option, int value) {
     case LB_OPT_TB_EDGE_PULL:
       if (value != 0 && value != 1) return fail(LB_EINVAL, "edge pull must be 0 (k_tb_pull) or 1 (in-kernel)");
       c->tb_edge_pull = value;
+      return LB_OK;
+    case LB_OPT_TB_TAIL_WEIGHT:
+      if (value != 0 && value != 1 && (value < 16 || value > 64))
+        return fail(LB_EINVAL, "tail weight (x16) must be 0 (auto), 1 (contiguous split) or in [16, 64]");
+      c->tb_tail_w16 = value;
       return LB_OK;
     case LB_OPT_FUSED_IMPL:
       if (value != 0 && value != 1) return fail(LB_EINVAL, "fused impl must be 0 (gather) or 1 (TMA)");

@@ -63,7 +63,8 @@
 #define LB_TB_STCS 0
 #endif
 // bit 0: BGK, bit 1: regularised — time-aligned work split (see the kernel;
-// default BGK: +0.7 % in two A/B runs on one box; regularised: -4.8 %)
+// BGK default, tuned wall / tail weights 21 / 17 x1/16: +6 % at 1920x2048;
+// regularised: -4.8 % with the contiguous split's weights, not retuned)
 #ifndef LB_TB_ALIGN
 #define LB_TB_ALIGN 1
 #endif
@@ -771,6 +772,10 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
   // preceded by TB_LEAD columns of weight, which the range holding that strip
   // start absorbs (unit_at maps T inside it to the strip start).
   constexpr int TB_LEAD = LB_TB_LEAD;
+  // wall_w16 packs the wall-strip weight (low 16 bits) and the tail weight
+  // (high 16 bits) of the aligned split, both x16
+  const int tail_w16 = wall_w16 >> 16;
+  wall_w16 &= 0xffff;
   auto strip_w = [&](int s) { return (nstrips > 1 && (s == 0 || s == nstrips - 1)) ? wall_w16 : 16; };
   // LB_TB_PAIR (variant, launched as clusters of 2 CTAs): the two CTAs of a
   // cluster sweep two vertically adjacent strips (a "virtual strip") over the
@@ -808,17 +813,30 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
   // E = ng - R nv remaining units share the columns [R c_v, lx) of every
   // virtual strip (tail region) by the weighted split above.
   constexpr bool ALIGN = (LB_TB_ALIGN >> (COLL == COLL_REGULARIZED ? 1 : 0)) & 1;
-  const int R_al = (ALIGN || paired) && nv > 1 ? ng / nv : 0;
+  const int R_al = ((ALIGN && tail_w16 >= 16) || paired) && nv > 1 ? ng / nv : 0;  // tail_w16 < 16: contiguous split
   const int E_al = ng - R_al * nv;
   const bool aligned = R_al >= 1 && E_al >= 1;
   const bool tail = aligned && gid >= R_al * nv;
+  // weighted work per main unit: the E tail units work at tail_w16 / 16 of
+  // the main units' rate, so a main unit takes W f / (E + f M) (f = tail
+  // factor, M = R nv main units) instead of the average W / (E + M)
   int64_t t16 = 0;
   for (int s = 0; s < nv; ++s) t16 += (int64_t)lx * vw(s);
-  t16 = (t16 + (int64_t)16 * TB_LEAD * (ng + nv)) / ng;  // weighted work per unit
-  auto main_cols = [&](int s) -> int {
-    const int c = (int)std::max<int64_t>(1, t16 / vw(s) - TB_LEAD);
+  t16 += (int64_t)16 * TB_LEAD * (ng + nv);
+  if (aligned) {
+    const int64_t f = tail_w16 >= 16 ? tail_w16 : 16;
+    t16 = t16 * f / (16 * (int64_t)E_al + f * R_al * nv);
+  }
+  // main-region columns per unit: two values (interior weight 16, the wall
+  // strips' weight), computed once — a 64-bit division per strip inside the
+  // tail loops below cost the tail CTAs ~15 us before their first load
+  // (two scalars, not an indexed array: that would live in local memory)
+  auto cols_for = [&](int w) -> int {
+    const int c = (int)std::max<int64_t>(1, t16 / w - TB_LEAD);
     return (int64_t)c * R_al >= lx ? (lx + R_al - 1) / R_al : c;
   };
+  const int cm_int = aligned ? cols_for(16) : 0, cm_wall = aligned ? cols_for(vw(0)) : 0;
+  auto main_cols = [&](int s) -> int { return vw(s) == 16 ? cm_int : cm_wall; };
   auto tail_lo = [&](int s) -> int { return tail ? std::min(lx, R_al * main_cols(s)) : 0; };
   if (aligned && !tail) {
     const int s = gid % nv, r = gid / nv, c = main_cols(s);

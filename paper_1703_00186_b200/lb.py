@@ -452,21 +452,24 @@ class Lattice:
         _check(lib().lb_set_option(self._ctx, 2, int(enable)))
 
     def temporal(self, enable: bool = True, grid: int = 0, l2_prefetch: int = 0, wall_weight16: int = 0,
-                 l2_promotion: int | None = None):
+                 l2_promotion: int | None = None, tail_weight16: int = 0):
         """Two steps per pass over HBM (LB_OPT_TEMPORAL, the default where it
         applies: fused mode, walls, N = 1 or N > 1 in peer mode, monitors on or
         off — with monitors the kernel reduces both states' invariants):
         lb_step advances pairs of steps with the two-step kernel.  grid: CTAs
         (0 = one per SM); l2_prefetch: L2 prefetch distance in columns (0 = off);
         wall_weight16: cost of a wall-strip column, x16, for the work split
-        (0 = the library default: 19 BGK, 20 regularised);
-        l2_promotion: L2 promotion of its TMA loads in bytes (None = library default)."""
+        (0 = the library default: 21 BGK (aligned split), 19 BGK (contiguous), 20 regularised);
+        l2_promotion: L2 promotion of its TMA loads in bytes (None = library default);
+        tail_weight16: cost of a tail-region column of the time-aligned (BGK) split,
+        x16 (0 = the library default, 17; 1 = the contiguous split instead)."""
         _check(lib().lb_set_option(self._ctx, 3, int(enable)))
         _check(lib().lb_set_option(self._ctx, 4, int(grid)))
         _check(lib().lb_set_option(self._ctx, 5, int(l2_prefetch)))
         _check(lib().lb_set_option(self._ctx, 6, int(wall_weight16)))
         if l2_promotion is not None:
             _check(lib().lb_set_option(self._ctx, 7, int(l2_promotion)))
+        _check(lib().lb_set_option(self._ctx, 9, int(tail_weight16)))
 
     def edge_pull(self, in_kernel: bool = True):
         """N > 1 two-step exchange: inside the kernel (edge CTAs wait and stage,

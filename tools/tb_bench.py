@@ -17,12 +17,12 @@ import lbgen  # noqa: E402
 import paper_1703_00186_b200 as lbm  # noqa: E402
 
 
-def run(lx, ly, tb, grid=0, l2=0, k=None, coll="bgk", ww=0, promo=None):
+def run(lx, ly, tb, grid=0, l2=0, k=None, coll="bgk", ww=0, promo=None, tw=0):
     k = k or int(os.environ.get("TB_K", "200"))
     s = torch.cuda.Stream()
     g = lbm.Lattice(lx, ly, collision=coll, stream=s, temporal=False)
     if tb:
-        g.temporal(True, grid=grid, l2_prefetch=l2, wall_weight16=ww, l2_promotion=promo)
+        g.temporal(True, grid=grid, l2_prefetch=l2, wall_weight16=ww, l2_promotion=promo, tail_weight16=tw)
     g.init_macro(*lbgen.rt_macro(lx, ly, 1.0 / 1.19697977039307435897239 ** 2))
     g.step(20)
     g.sync()
@@ -60,6 +60,11 @@ def main():
         grid, ww = (int(v) for v in combo.split(":"))
         ms, ml, out = run(lx, ly, True, grid, 0, ww=ww)
         print(json.dumps({"tb": 1, "grid": grid, "wall_w16": ww, "ms_per_step": ms, "mlups": ml,
+                          "bit_identical": bool(np.array_equal(out, ref))}), flush=True)
+    for combo in [x for x in os.environ.get("TB_WT", "").split(",") if x]:  # wall:tail weights x16
+        ww, tw = (int(v) for v in combo.split(":"))
+        ms, ml, out = run(lx, ly, True, 0, 0, ww=ww, tw=tw)
+        print(json.dumps({"tb": 1, "wall_w16": ww, "tail_w16": tw, "ms_per_step": ms, "mlups": ml,
                           "bit_identical": bool(np.array_equal(out, ref))}), flush=True)
     promos = [int(x) for x in os.environ.get("TB_PROMO", "").split(",") if x]
     if promos:

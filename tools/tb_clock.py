@@ -1,6 +1,6 @@
 """Per-CTA timeline of one two-step launch (tools only).
 
-LB_D2Q37_LIB=paper_1703_00186_b200/variants/liblb_<tag>.so python tools/tb_clock.py [lx ly] [out.json]
+LB_D2Q37_LIB=paper_1703_00186_b200/variants/liblb_<tag>.so [TB_WW=w16] python tools/tb_clock.py [lx ly] [out.json]
 
 The variant must be built with LB_TB_CLOCK=1 (tools/build_tb_variant.py 104 1 1
 LB_TB_CLOCK=1): every CTA of k_step2_tb records %globaltimer at its start and
@@ -29,6 +29,9 @@ def main():
     res = {"lx": lx, "ly": ly, "launches": []}
     for coll in ("bgk", "regularized"):
         g = lbm.Lattice(lx, ly, collision=coll, temporal=True)
+        if os.environ.get("TB_WW") or os.environ.get("TB_TW"):  # wall-strip / tail weights x16 (work split)
+            g.temporal(True, wall_weight16=int(os.environ.get("TB_WW", "0")),
+                       tail_weight16=int(os.environ.get("TB_TW", "0")))
         g.init_macro(*lbgen.rt_macro(lx, ly, 1.0 / 1.19697977039307435897239 ** 2))
         g.step(40)
         g.sync()

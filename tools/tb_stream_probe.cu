@@ -324,6 +324,33 @@ __global__ void __launch_bounds__(NCONS + 32, 1)
   }
 }
 
+// Stores alone, the kernel's pattern (37 x 104-row runs per output column of a
+// strip), issued by NW warps per CTA: 4 = the kernel (one row per thread, 37
+// stores), 8 / 16 = the populations split between 2 / 4 warp groups.
+template <int NW>
+__global__ void __launch_bounds__(NW * 32, 1) k_store_only(double* __restrict__ B, int lx, int ly, int nyp, int ns) {
+  constexpr int GROUPS = NW / 4;
+  const int tid = threadIdx.x, row = tid & 127, grp = tid >> 7;
+  const int64_t cs = (int64_t)Q * nyp;
+  const int64_t U = (int64_t)ns * lx;
+  int64_t u = U * blockIdx.x / gridDim.x;
+  const int64_t ue = U * (blockIdx.x + 1) / gridDim.x;
+  const double v = 1.0 + tid;
+  while (u < ue) {
+    const int s = (int)(u / lx), x0 = (int)(u % lx);
+    const int x1 = (int)std::min<int64_t>(lx, x0 + (ue - u));
+    u += x1 - x0;
+    const int ya = strip_ya(s, ns, ly);
+    if (row < HT && ya + row < ly)
+      for (int c = x0; c < x1; ++c) {
+        double* p = B + (int64_t)(H + c) * cs + Y0 + ya + row;
+#pragma unroll
+        for (int l = 0; l < Q; ++l)
+          if (l % GROUPS == grp) p[(int64_t)l * nyp] = v;
+      }
+  }
+}
+
 __global__ void k_copy(const double2* __restrict__ a, double2* __restrict__ b, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     b[i] = a[i];
@@ -412,6 +439,20 @@ int main(int argc, char** argv) {
       }
     }
   };
+  if (getenv("PROBE_STORES")) {
+    double ld_bytes, st_bytes;
+    req(nsm, 0, ld_bytes, st_bytes);
+    auto run = [&](auto kern, int nw, int grid) {
+      const double ms = timeit([&] { kern<<<grid, nw * 32>>>(B, lx, ly, nyp, ns); });
+      printf("{\"probe\": \"stores only\", \"warps_per_cta\": %d, \"ctas\": %d, \"ms\": %.4f, \"gbs\": %.1f}\n", nw,
+             grid, ms, st_bytes / ms * 1e-6);
+    };
+    run(k_store_only<4>, 4, nsm);
+    run(k_store_only<8>, 8, nsm);
+    run(k_store_only<16>, 16, nsm);
+    run(k_store_only<4>, 4, 4 * nsm);
+    return 0;
+  }
   const double ms_copy = timeit([&] { k_copy<<<nsm * 8, 512>>>((const double2*)A, (double2*)B, n / 2); });
   printf("{\"probe\": \"double2 copy\", \"ms\": %.4f, \"gbs\": %.1f}\n", ms_copy, 2.0 * n * 8 / ms_copy * 1e-6);
   const char* sname[4] = {"stg", "bulk", "loads only", "stores only"};
