@@ -342,8 +342,8 @@ int lb_sync(lb_ctx* ctx);
  * fused steps; an odd remainder takes one fused step.  LB_OPT_TB_GRID: CTAs of
  * that kernel (0 = one per SM), LB_OPT_TB_L2_PREFETCH: L2 prefetch distance in
  * columns (0 = off, the default, <= 64; per-line prefetch of the newest column).  LB_OPT_TB_WALL_WEIGHT: cost of a column of a
- * wall strip relative to an interior one, x16 (work split; 0 = the default: 21 for BGK with the
- * aligned split, 19 with the contiguous one, 20 for the regularised collide).
+ * wall strip relative to an interior one, x16 (work split; 0 = the default: 21 with the
+ * time-aligned split, with the contiguous one 19 for BGK and 20 for the regularised collide).
  * LB_OPT_TB_L2_PROMOTION: L2 promotion of that kernel's TMA window loads in
  * bytes (0 = none, 64 = default, 128, 256); results do not depend on it.
  * LB_OPT_TB_EDGE_PULL (N > 1, peer mode): 1 (default) = the exchange runs
@@ -353,7 +353,7 @@ int lb_sync(lb_ctx* ctx);
  * overlap the exchange (§8a6); 0 = a separate k_tb_pull launch
  * (wait for both neighbours, stage whole columns) before the kernel.  Both
  * give the same bits.
- * LB_OPT_TB_TAIL_WEIGHT: the BGK two-step kernel splits its work
+ * LB_OPT_TB_TAIL_WEIGHT: the two-step kernel splits its work
  * time-aligned (every strip's main region cut into the same column ranges, the
  * CTAs left over share the remaining columns of every strip: the tail); the
  * cost of a tail column relative to a main-region one, x16 (0 = the default,

@@ -858,17 +858,15 @@ static bool tb_usable(const lb_ctx* c) {
 // two-step kernel's work split: measured per-CTA times (tools/tb_clock.py,
 // 1920x2048) give 1.17 (BGK) and 1.25 (regularised) per iteration, and a
 // sweep of the BGK weight 17..21 peaks at 19.
-// BGK uses the time-aligned split (LB_OPT_TB_TAIL_WEIGHT != 1), where a
-// wall-strip column costs 1.28x an interior one (per-CTA clocks: 1.92 vs 1.50
-// us per iteration) and a weight sweep (tools/gpu_job_r02_wt.sh) peaks at
-// wall 21 / tail 17 (x1/16); with the contiguous split 19 (BGK) and 20
-// (regularised) balance best.
-static bool tb_aligned(const lb_ctx* c) {
-  return c->p.collision != LB_COLLIDE_REGULARIZED && c->tb_tail_w16 != 1;
-}
+// Both collides use the time-aligned split (LB_OPT_TB_TAIL_WEIGHT != 1),
+// where a wall-strip column costs ~1.3x an interior one (per-CTA clocks, BGK:
+// 1.92 vs 1.50 us per iteration) and weight sweeps (tools/gpu_job_r02_wt.sh,
+// gpu_job_r02_wtreg.sh) peak at wall 21 / tail 17 (x1/16) for both; with the
+// contiguous split 19 (BGK) and 20 (regularised) balance best.
+static bool tb_aligned(const lb_ctx* c) { return c->tb_tail_w16 != 1; }
 static int tb_wall_weight(const lb_ctx* c) {
   if (c->tb_wall_w16 > 0) return c->tb_wall_w16;
-  return c->p.collision == LB_COLLIDE_REGULARIZED ? 20 : tb_aligned(c) ? 21 : 19;
+  return tb_aligned(c) ? 21 : c->p.collision == LB_COLLIDE_REGULARIZED ? 20 : 19;
 }
 // The kernel's split parameter: wall weight | tail weight << 16 (both x16;
 // tail 0: the contiguous split).

@@ -62,11 +62,11 @@
 #ifndef LB_TB_STCS
 #define LB_TB_STCS 0
 #endif
-// bit 0: BGK, bit 1: regularised — time-aligned work split (see the kernel;
-// BGK default, tuned wall / tail weights 21 / 17 x1/16: +6 % at 1920x2048;
-// regularised: -4.8 % with the contiguous split's weights, not retuned)
+// bit 0: BGK, bit 1: regularised — the time-aligned work split can be used
+// (see the kernel; the host's default, with wall / tail weights 21 / 17
+// x1/16: BGK +7.6 %, regularised +3.4 % at 1920x2048)
 #ifndef LB_TB_ALIGN
-#define LB_TB_ALIGN 1
+#define LB_TB_ALIGN 3
 #endif
 // clusters of 2 CTAs sweeping adjacent strips in lockstep (see the kernel;
 // variant builds only: -3 %, the per-iteration cluster barrier costs more than

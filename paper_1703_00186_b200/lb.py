@@ -459,9 +459,9 @@ class Lattice:
         lb_step advances pairs of steps with the two-step kernel.  grid: CTAs
         (0 = one per SM); l2_prefetch: L2 prefetch distance in columns (0 = off);
         wall_weight16: cost of a wall-strip column, x16, for the work split
-        (0 = the library default: 21 BGK (aligned split), 19 BGK (contiguous), 20 regularised);
+        (0 = the library default: 21 with the time-aligned split; contiguous: 19 BGK, 20 regularised);
         l2_promotion: L2 promotion of its TMA loads in bytes (None = library default);
-        tail_weight16: cost of a tail-region column of the time-aligned (BGK) split,
+        tail_weight16: cost of a tail-region column of the time-aligned split,
         x16 (0 = the library default, 17; 1 = the contiguous split instead)."""
         _check(lib().lb_set_option(self._ctx, 3, int(enable)))
         _check(lib().lb_set_option(self._ctx, 4, int(grid)))

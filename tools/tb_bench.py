@@ -61,10 +61,13 @@ def main():
         ms, ml, out = run(lx, ly, True, grid, 0, ww=ww)
         print(json.dumps({"tb": 1, "grid": grid, "wall_w16": ww, "ms_per_step": ms, "mlups": ml,
                           "bit_identical": bool(np.array_equal(out, ref))}), flush=True)
+    wt_coll = os.environ.get("TB_WT_COLL", "bgk")
+    if wt_coll != "bgk" and os.environ.get("TB_WT"):
+        _, _, ref = run(lx, ly, False, coll=wt_coll)
     for combo in [x for x in os.environ.get("TB_WT", "").split(",") if x]:  # wall:tail weights x16
         ww, tw = (int(v) for v in combo.split(":"))
-        ms, ml, out = run(lx, ly, True, 0, 0, ww=ww, tw=tw)
-        print(json.dumps({"tb": 1, "wall_w16": ww, "tail_w16": tw, "ms_per_step": ms, "mlups": ml,
+        ms, ml, out = run(lx, ly, True, 0, 0, ww=ww, tw=tw, coll=wt_coll)
+        print(json.dumps({"tb": 1, "coll": wt_coll, "wall_w16": ww, "tail_w16": tw, "ms_per_step": ms, "mlups": ml,
                           "bit_identical": bool(np.array_equal(out, ref))}), flush=True)
     promos = [int(x) for x in os.environ.get("TB_PROMO", "").split(",") if x]
     if promos:
