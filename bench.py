@@ -362,8 +362,12 @@ def main():
     launches = g.launch_count() - launches0
     ms = max_over_ranks(e0.elapsed_time(e1))
     # ---- the dominant kernel's launch durations (CUDA events per launch on the
-    # launch stream), right after the headline region: the same clocks and
-    # power state as the headline, before the repetitions heat the board
+    # launch stream), right after the headline region, after one idle second:
+    # a sustained run of the two-step kernel reaches the board's power limit
+    # within ~1 s and the SM clock falls (DESIGN.md §6 "Power"); an idle second
+    # restores it, so this region starts from the headline's power state
+    # instead of inheriting the heat of the headline region
+    time.sleep(1.0)
     g.profile(True)
     g.profile_reset()
     barrier()
