@@ -71,6 +71,13 @@
 // clusters of 2 CTAs sweeping adjacent strips in lockstep (see the kernel;
 // variant builds only: -3 %, the per-iteration cluster barrier costs more than
 // the 208-row store runs gain)
+// phase-2 warp rotation (see the kernel; 0 = warp NW1 + k handles row block k).
+// Measured neutral (rotations 0 / 1 / 2 at the tuned weights: 17.85K / 17.79K /
+// 17.83K, then 17.65K / 17.81K / 17.77K): the wall strips' extra cost is not
+// scheduler contention.  Variant builds only.
+#ifndef LB_TB_P2ROT
+#define LB_TB_P2ROT 0
+#endif
 #ifndef LB_TB_PAIR
 #define LB_TB_PAIR 0
 #endif
@@ -761,6 +768,15 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
   const uint32_t bar_cp = smem_u32(bars + NB + 4);  // TMEM: copies of phase-1 item k done: bar_cp + 8 (k & 1)
   // TMEM: this phase-2 warp's lane quarter
   const uint32_t tlane = tbase + ((uint32_t)(32 * (warp & 3)) << 16);
+  // phase-2 warp w handles the strip rows of block (w - NW1 + P2ROT) mod NW2:
+  // rotated so that the warps holding the wall band rows of the two phases
+  // (the thermal repopulation and the virtual-row copies) sit on different
+  // schedulers (warp w issues on scheduler w mod 4: unrotated, phase 1's
+  // rows [ya-3, ya+29) and phase 2's [ya, ya+32) both land on scheduler 0 at
+  // the bottom wall, and on scheduler 3 at the top wall).  TMEM: a warp reads
+  // only its own lane quarter, so no rotation.
+  constexpr int P2ROT = TMEM ? 0 : LB_TB_P2ROT;
+  const int p2row = 32 * ((warp - C::NW1 + P2ROT) % C::NW2) + (tid & 31);
 
   // Weighted split: a column of a wall strip costs wall_w16 / 16 of an interior
   // one (thermal repopulation and mirror copies on its wall warps), so the CTAs
@@ -1089,7 +1105,7 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
       } else if (NBAR) {
         // phase 2 (named-barrier hand-over): wait until phase 1 wrote t - 1, gather, release
         if (t > 0) asm volatile("bar.sync %0, %1;" ::"r"(3 + ((t - 1) & 1)), "r"(C::NT) : "memory");
-        const int i = tid - 32 * C::NW1;
+        const int i = p2row;
         const int y = ya + i;
         const bool valid = t >= 7 && i < HT && y < ly;
         double f[Q];
@@ -1100,7 +1116,7 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
       } else if (DECOUPLE) {
         // phase 2 (decoupled): wait for item I - 1, gather, release the slots
         if (t > 0) mbar_wait(bar_full + 8 * ((I - 1) & 1), ((I - 1) >> 1) & 1);
-        const int i = tid - 32 * C::NW1;
+        const int i = p2row;
         const int y = ya + i;
         const bool valid = t >= 7 && i < HT && y < ly;
         double f[Q];
@@ -1112,7 +1128,7 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
         // phase 2, offset against phase 1: collide right after the barrier
         // (only the 3 newest populations still to load), then gather the
         // next column's older populations after the stores
-        const int i = tid - 32 * C::NW1;
+        const int i = p2row;
         const int y = ya + i;
         const bool valid = i < HT && y < ly;
         if (t >= 7) {
@@ -1131,7 +1147,7 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
             mbar_wait(bar_cp + 8 * (k & 1), (k >> 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           });
-          const int i = tid - 32 * C::NW1;
+          const int i = p2row;
           const int y = ya + i;
           if (i < HT && y < ly)
             phase2_update<COLL, MON>(f, B, g, y, xs - 7 + t, thermal, r, y >= own_lo && y < own_hi, acc, !peers);
@@ -1139,7 +1155,7 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       } else if (t >= 7) {
         // phase 2: state n+2 at column c2 = xs - 7 + t, rows [ya, ya+HT)
-        const int i = tid - 32 * C::NW1;
+        const int i = p2row;
         const int y = ya + i;
         if (i < HT && y < ly)
           phase2<COLL, R1, MON>(s1, B, g, t, i, y, xs - 7 + t, thermal, r, y >= own_lo && y < own_hi, acc,
