@@ -358,7 +358,13 @@ int lb_sync(lb_ctx* ctx);
  * CTAs left over share the remaining columns of every strip: the tail); the
  * cost of a tail column relative to a main-region one, x16 (0 = the default,
  * measured: 17; 16..64), or 1 = the contiguous split instead (strip-major
- * column ranges).  Work split only: results do not depend on it. */
+ * column ranges).  Work split only: results do not depend on it.
+ * LB_OPT_TB_PDL (1 = default, 0 = off): the two-step kernel is launched with
+ * programmatic dependent launch, so its CTAs start (and compute their work
+ * split) on the SMs the previous launch's CTAs free; each waits for the
+ * previous grid's completion before touching global memory.  Same results.
+ * Not used with peers (N > 1): ranks sharing one GPU (tests) would park CTAs
+ * of their next launch on SMs a waiting neighbour needs. */
 enum lb_option {
   LB_OPT_PROPAGATE_IMPL = 0,
   LB_OPT_FUSED_IMPL = 1,
@@ -369,7 +375,8 @@ enum lb_option {
   LB_OPT_TB_WALL_WEIGHT = 6,
   LB_OPT_TB_L2_PROMOTION = 7,
   LB_OPT_TB_EDGE_PULL = 8,
-  LB_OPT_TB_TAIL_WEIGHT = 9
+  LB_OPT_TB_TAIL_WEIGHT = 9,
+  LB_OPT_TB_PDL = 10
 };
 int lb_set_option(lb_ctx* ctx, int option, int value);
 

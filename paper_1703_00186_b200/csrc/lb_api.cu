@@ -151,6 +151,7 @@ struct lb_ctx {
   int tb_promo = 64;            // LB_OPT_TB_L2_PROMOTION: L2 promotion of its TMA loads (bytes)
   int tb_wall_w16 = 0;          // LB_OPT_TB_WALL_WEIGHT: wall-strip column cost x16 (work split; 0 = per collision)
   int tb_tail_w16 = 0;          // LB_OPT_TB_TAIL_WEIGHT: tail-region column cost x16 (aligned split; 0 = default)
+  int tb_pdl = 1;               // LB_OPT_TB_PDL: programmatic dependent launch of the two-step kernel
   int tb_edge_pull = 1;         // LB_OPT_TB_EDGE_PULL: N > 1 two-step exchange inside the kernel (1) or k_tb_pull first (0)
   double* d_stage = nullptr;    // N > 1 two-step: the neighbours' 6 edge columns (2 x 6 x cs doubles)
   unsigned int* d_ctas = nullptr;  // N > 1 two-step, in-kernel exchange: finished-CTA count (kept zero)
@@ -910,7 +911,9 @@ static int step_tb(lb_ctx* c) {
   }
   TRY(launch(c, c->p.collision ? "k_step2_tb_reg" : "k_step2_tb", c->s, 2 * c->L.sites, [&] {
     return lbk::launch_step2_tb(c->g, c->tb, c->par, c->B, c->p.bc_y, c->p.collision, c->relax, grid, c->tb_l2,
-                                tb_split_weights(c), mon, peers ? 1 : 0, inpull ? &pull : nullptr, c->s);
+                                tb_split_weights(c), mon, peers ? 1 : 0, inpull ? &pull : nullptr, c->s,
+                                c->tb_pdl != 0 && !peers);  // (peers: ranks sharing a GPU in tests must not
+                                                            // park next-launch CTAs on SMs a neighbour needs)
   }));
   if (peers) {  // publish: this launch is complete (the neighbours may now read our new state)
     c->peer_step += 1;
@@ -1202,6 +1205,10 @@ int lb_set_option(lb_ctx* c, int option, int value) {
     case LB_OPT_TB_EDGE_PULL:
       if (value != 0 && value != 1) return fail(LB_EINVAL, "edge pull must be 0 (k_tb_pull) or 1 (in-kernel)");
       c->tb_edge_pull = value;
+      return LB_OK;
+    case LB_OPT_TB_PDL:
+      if (value != 0 && value != 1) return fail(LB_EINVAL, "PDL must be 0 or 1");
+      c->tb_pdl = value;
       return LB_OK;
     case LB_OPT_TB_TAIL_WEIGHT:
       if (value != 0 && value != 1 && (value < 16 || value > 64))

@@ -147,9 +147,12 @@ struct TbPeer {
 // peers != 0: columns beyond the slab come from the staging buffer (N > 1) and
 // B's halo is not written; else the N = 1 periodic wrap.
 // pull != nullptr (peers only): in-kernel edge pulls instead of a preceding launch_tb_pull.
+// pdl: launch with programmatic dependent launch (the kernel's prologue may
+// overlap the previous kernel's last CTAs; griddepcontrol.wait before any
+// global-memory access).
 cudaError_t launch_step2_tb(const Geo& g, const TbMaps* t, int src_buf, double* B, int bc, int coll,
                             const lbd::Relax& r, int grid, int l2_dist, int wall_w16, double* mon, int peers,
-                            const TbPeer* pull, cudaStream_t s);
+                            const TbPeer* pull, cudaStream_t s, bool pdl = false);
 // CTAs a two-step launch with `grid` requested actually uses
 int tb_grid(const Geo& g, int grid);
 // this rank's counter += 1 (system-scope release), after the step kernel

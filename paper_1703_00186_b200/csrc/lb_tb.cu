@@ -739,6 +739,10 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
                         ((LB_TB_SKEW >> (COLL == COLL_REGULARIZED ? 1 : 0)) & 1);
   static_assert(!TMEM || (EARLY && !DECOUPLE && !NBAR), "TMEM ring: CTA barrier per iteration, early refill");
   static_assert(!TMEM || C::NW2 == 4, "TMEM ring: one phase-2 warp per TMEM lane quarter");
+  // programmatic dependent launch (host option): the next launch may start
+  // its CTAs (on SMs this launch frees) and run its prologue; it waits at
+  // griddepcontrol.wait below for this grid's completion and memory
+  asm volatile("griddepcontrol.launch_dependents;");
   extern __shared__ __align__(128) double sm[];
   double* s0 = sm;
   double* s1 = sm + C::S0_DBL;  // the ring, or (TMEM) the two staging buffers
@@ -898,6 +902,9 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
   const uint32_t bar_full = smem_u32(bars + NB), bar_empty = smem_u32(bars + NB + 2);
   double acc[5] = {0.0, 0.0, 0.0, 0.0, INFINITY};  // MON: this thread's state (n+1 or n+2)
   bool cl_armed = false;  // PAIR: a cluster-barrier arrival is pending
+  // everything above touched only kernel parameters and shared memory: from
+  // here on global memory (the previous launch's output, the buffer it read)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   while (u < u_end) {
     const int vstrip = (int)(u / lx);
@@ -1268,7 +1275,7 @@ bool encode(CUtensorMap* m, double* base, const Geo& g, int box_rows, int box_po
 template <int COLL, bool MON>
 cudaError_t launch_tb(const Geo& g, const TbMaps* t, int src_buf, double* B, const Relax& r, int grid,
                       int l2_dist, int thermal, int wall_w16, double* mon, int peers, const TbPeer* pull,
-                      cudaStream_t s) {
+                      cudaStream_t s, bool pdl) {
   auto kern = k_step2_tb<COLL, TB_HT, TB_PF, MON>;
   static unsigned long long done_mask = 0;  // opt-in smem is a per-device attribute
   int dev = 0;
@@ -1307,6 +1314,21 @@ cudaError_t launch_tb(const Geo& g, const TbMaps* t, int src_buf, double* B, con
     return cudaLaunchKernelEx(&cfg, kern, km, B, g, r, nstr, l2_dist, thermal, wall_w16, mon, peers, asrc, pp, ip);
   }
 #endif
+  if (pdl) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)tb_grid(g, grid));
+    cfg.blockDim = dim3(Cfg::NT);
+    cfg.dynamicSmemBytes = Cfg::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const double* asrc = t->bufs[src_buf];
+    const int nstr = (g.ly + TB_HT - 1) / TB_HT, ip = inpull ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, km, B, g, r, nstr, l2_dist, thermal, wall_w16, mon, peers, asrc, pp, ip);
+  }
   kern<<<tb_grid(g, grid), Cfg::NT, Cfg::SMEM, s>>>(km, B, g, r, (g.ly + TB_HT - 1) / TB_HT, l2_dist, thermal,
                                                     wall_w16, mon, peers, t->bufs[src_buf], pp,
                                                     inpull ? 1 : 0);
@@ -1367,16 +1389,16 @@ cudaError_t tb_upload_constants(const double* k_bottom, const double* k_top, con
 
 cudaError_t launch_step2_tb(const Geo& g, const TbMaps* t, int src_buf, double* B, int bc, int coll,
                             const Relax& r, int grid, int l2_dist, int wall_w16, double* mon, int peers,
-                            const TbPeer* pull, cudaStream_t s) {
+                            const TbPeer* pull, cudaStream_t s, bool pdl) {
   if (bc != BC_THERMAL && bc != BC_ADIABATIC) return cudaErrorNotSupported;
   const int th = bc == BC_THERMAL;
   if (mon)
     return coll == COLL_REGULARIZED
-               ? launch_tb<COLL_REGULARIZED, true>(g, t, src_buf, B, r, grid, l2_dist, th, wall_w16, mon, peers, pull, s)
-               : launch_tb<COLL_BGK, true>(g, t, src_buf, B, r, grid, l2_dist, th, wall_w16, mon, peers, pull, s);
+               ? launch_tb<COLL_REGULARIZED, true>(g, t, src_buf, B, r, grid, l2_dist, th, wall_w16, mon, peers, pull, s, pdl)
+               : launch_tb<COLL_BGK, true>(g, t, src_buf, B, r, grid, l2_dist, th, wall_w16, mon, peers, pull, s, pdl);
   return coll == COLL_REGULARIZED
-             ? launch_tb<COLL_REGULARIZED, false>(g, t, src_buf, B, r, grid, l2_dist, th, wall_w16, mon, peers, pull, s)
-             : launch_tb<COLL_BGK, false>(g, t, src_buf, B, r, grid, l2_dist, th, wall_w16, mon, peers, pull, s);
+             ? launch_tb<COLL_REGULARIZED, false>(g, t, src_buf, B, r, grid, l2_dist, th, wall_w16, mon, peers, pull, s, pdl)
+             : launch_tb<COLL_BGK, false>(g, t, src_buf, B, r, grid, l2_dist, th, wall_w16, mon, peers, pull, s, pdl);
 }
 
 // ---- N > 1: staging of the neighbours' edge columns (peer memory -> local)

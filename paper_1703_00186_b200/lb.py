@@ -452,7 +452,7 @@ class Lattice:
         _check(lib().lb_set_option(self._ctx, 2, int(enable)))
 
     def temporal(self, enable: bool = True, grid: int = 0, l2_prefetch: int = 0, wall_weight16: int = 0,
-                 l2_promotion: int | None = None, tail_weight16: int = 0):
+                 l2_promotion: int | None = None, tail_weight16: int = 0, pdl: bool | None = None):
         """Two steps per pass over HBM (LB_OPT_TEMPORAL, the default where it
         applies: fused mode, walls, N = 1 or N > 1 in peer mode, monitors on or
         off — with monitors the kernel reduces both states' invariants):
@@ -462,7 +462,8 @@ class Lattice:
         (0 = the library default: 21 with the time-aligned split; contiguous: 19 BGK, 20 regularised);
         l2_promotion: L2 promotion of its TMA loads in bytes (None = library default);
         tail_weight16: cost of a tail-region column of the time-aligned split,
-        x16 (0 = the library default, 17; 1 = the contiguous split instead)."""
+        x16 (0 = the library default, 17; 1 = the contiguous split instead);
+        pdl: programmatic dependent launch of the kernel (None = library default, on)."""
         _check(lib().lb_set_option(self._ctx, 3, int(enable)))
         _check(lib().lb_set_option(self._ctx, 4, int(grid)))
         _check(lib().lb_set_option(self._ctx, 5, int(l2_prefetch)))
@@ -470,6 +471,8 @@ class Lattice:
         if l2_promotion is not None:
             _check(lib().lb_set_option(self._ctx, 7, int(l2_promotion)))
         _check(lib().lb_set_option(self._ctx, 9, int(tail_weight16)))
+        if pdl is not None:
+            _check(lib().lb_set_option(self._ctx, 10, int(bool(pdl))))
 
     def edge_pull(self, in_kernel: bool = True):
         """N > 1 two-step exchange: inside the kernel (edge CTAs wait and stage,

@@ -22,7 +22,9 @@ def run(lx, ly, tb, grid=0, l2=0, k=None, coll="bgk", ww=0, promo=None, tw=0):
     s = torch.cuda.Stream()
     g = lbm.Lattice(lx, ly, collision=coll, stream=s, temporal=False)
     if tb:
-        g.temporal(True, grid=grid, l2_prefetch=l2, wall_weight16=ww, l2_promotion=promo, tail_weight16=tw)
+        pdl = os.environ.get("TB_PDL")  # programmatic dependent launch on / off (unset: library default)
+        g.temporal(True, grid=grid, l2_prefetch=l2, wall_weight16=ww, l2_promotion=promo, tail_weight16=tw,
+                   pdl=None if pdl is None else bool(int(pdl)))
     g.init_macro(*lbgen.rt_macro(lx, ly, 1.0 / 1.19697977039307435897239 ** 2))
     g.step(20)
     g.sync()
