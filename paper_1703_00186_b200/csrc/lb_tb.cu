@@ -375,6 +375,28 @@ __device__ __forceinline__ double checked_rho(const Macro& m) {
   return chk != chk ? -INFINITY : m.rho;
 }
 
+#ifndef LB_TB_MON_BRANCHLESS  // monitors accumulated without branches inside the collision (see below)
+#define LB_TB_MON_BRANCHLESS 1
+#endif
+// Branch-free form (LB_TB_MON_BRANCHLESS): the owned-site test and the body
+// force enter as factors, so the hook adds no branch in the middle of the
+// collision (a branch there ends the basic block the compiler schedules the
+// relaxation in).  w = 1 for an owned site, 0 otherwise; without a body force
+// the increments are exact zeros, so the sums equal the branched form's
+// (w m.rho + a is exact for w in {0, 1}).
+__device__ __forceinline__ void acc_invariants_w(const Macro& m, const Relax& r, double w, double (&a)[5]) {
+  const double djx = __dmul_rn(r.omega, __dmul_rn(m.rho, r.tgx));
+  const double djy = __dmul_rn(r.omega, __dmul_rn(m.rho, r.tgy));
+  const double tg2 = __fma_rn(r.tgx, r.tgx, __dmul_rn(r.tgy, r.tgy));
+  const double dE = __dmul_rn(r.omega, __fma_rn(m.jx, r.tgx, __fma_rn(m.jy, r.tgy,
+                                                    __dmul_rn(m.rho, __fma_rn(0.5, tg2, r.dT)))));
+  a[0] = __fma_rn(w, m.rho, a[0]);
+  a[1] = __fma_rn(w, __dadd_rn(m.jx, djx), a[1]);
+  a[2] = __fma_rn(w, __dadd_rn(m.jy, djy), a[2]);
+  a[3] = __fma_rn(w, __fma_rn(0.5, m.e, dE), a[3]);
+  a[4] = fmin(a[4], w != 0.0 ? checked_rho(m) : INFINITY);
+}
+
 __device__ __forceinline__ void acc_invariants(const Macro& m, const Relax& r, double (&a)[5]) {
   if (r.tgx == 0.0 && r.tgy == 0.0 && r.dT == 0.0) {
     // no body force (uniform branch): the increments below are exact zeros
@@ -438,7 +460,8 @@ __device__ __forceinline__ void phase1_collide(double (&f)[Q], int y, int ly, bo
   if (thermal && (y < 3 || y >= ly - 3)) thermal_wall(f, y < 3 ? 0 : 1);
   // monitors: accumulated as soon as the collision has formed the moments
   auto hook = [&](const Macro& m) {
-    if (MON && own) acc_invariants(m, r, acc);
+    if (MON && LB_TB_MON_BRANCHLESS) acc_invariants_w(m, r, own ? 1.0 : 0.0, acc);
+    else if (MON && own) acc_invariants(m, r, acc);
   };
   tb_collide<COLL>(f, r, hook);
 }
@@ -509,7 +532,8 @@ __device__ __forceinline__ void phase2_update(double (&f)[Q], double* __restrict
   const int ly = g.ly;
   if (thermal && (y < 3 || y >= ly - 3)) thermal_wall(f, y < 3 ? 0 : 1);
   auto hook = [&](const Macro& m) {
-    if (MON && own) acc_invariants(m, r, acc);
+    if (MON && LB_TB_MON_BRANCHLESS) acc_invariants_w(m, r, own ? 1.0 : 0.0, acc);
+    else if (MON && own) acc_invariants(m, r, acc);
   };
   tb_collide<COLL>(f, r, hook);
   // 64-bit stride: one IMAD.WIDE per store instead of IMAD + LEA + LEA.HI.X
