@@ -1099,7 +1099,8 @@ int lb_invariants_pair_async(lb_ctx* c, double* host_out) {
   double* res = c->d_part + lbk::invariants_scratch(c->g);  // 2 x 5 doubles of device result space
   const int G = c->mon_tb_G;
   TRY(launch(c, "k_monitor_reduce_pair", c->s, 0, [&] {
-    return lbk::launch_monitor_reduce_pair(c->d_mon_tb, G, mapped ? mapped : res, c->d_nonphys, c->s);
+    return lbk::launch_monitor_reduce_pair(c->d_mon_tb, G, mapped ? mapped : res, c->d_nonphys, c->s,
+                                           c->tb_pdl != 0 && !c->peers_on);
   }));
   if (!mapped) CU(cudaMemcpyAsync(host_out, res, 10 * sizeof(double), cudaMemcpyDeviceToHost, c->s));
   return LB_OK;

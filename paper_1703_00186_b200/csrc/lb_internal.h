@@ -69,7 +69,7 @@ cudaError_t launch_monitor_reduce(const double* mon, int64_t nslots, double* par
                                   double* out, unsigned int* flag, cudaStream_t s);
 // Two slot sets (nslots each, consecutive) reduced by one block into out[10].
 cudaError_t launch_monitor_reduce_pair(const double* mon, int64_t nslots, double* out, unsigned int* flag,
-                                       cudaStream_t s);
+                                       cudaStream_t s, bool pdl = false);
 // TMA-staged kernels (lb_tma.cu): tensor maps of both buffers, built once.
 // Buffer k viewed as {nyp rows, 37 populations, nx columns}, box {256, 1, 1}.
 struct TmaMaps {

@@ -688,8 +688,13 @@ __global__ void __launch_bounds__(RED_TPB) k_monitor_reduce(const double* __rest
 
 // Both states of a two-step launch in ONE single-block launch (nslots per
 // set, set 1 at mon + 5 nslots): out[0..4] = set 0, out[5..9] = set 1.
+// Launched with programmatic dependent launch after the two-step kernel
+// (pdl): it may start while that kernel drains and waits for it before
+// reading the partials; the next two-step launch may start during it.
 __global__ void __launch_bounds__(RED_TPB) k_monitor_reduce_pair(const double* __restrict__ mon, int nslots,
                                                                  double* out, unsigned int* flag) {
+  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   __shared__ double sm[5 * RED_TPB];
   const int t = threadIdx.x;
   for (int set = 0; set < 2; ++set) {
@@ -712,7 +717,19 @@ __global__ void __launch_bounds__(RED_TPB) k_monitor_reduce_pair(const double* _
 }
 
 cudaError_t launch_monitor_reduce_pair(const double* mon, int64_t nslots, double* out, unsigned int* flag,
-                                       cudaStream_t s) {
+                                       cudaStream_t s, bool pdl) {
+  if (pdl) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(1);
+    cfg.blockDim = dim3(RED_TPB);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_monitor_reduce_pair, mon, (int)nslots, out, flag);
+  }
   k_monitor_reduce_pair<<<1, RED_TPB, 0, s>>>(mon, (int)nslots, out, flag);
   return cudaGetLastError();
 }

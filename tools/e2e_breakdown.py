@@ -4,6 +4,7 @@ bandwidth, lb_set_state, K steps with and without monitors, lb_gather.
 usage (GPU box): python tools/e2e_breakdown.py [K]
 """
 import json
+import os
 import sys
 import time
 
@@ -38,6 +39,8 @@ res["raw_d2h_gbs"] = round(n * 8 / res["raw_d2h_ms"] / 1e6, 1)
 del dev
 
 g = lb.Lattice(LX, LY, tau=0.8, t_bottom=1.02, t_top=0.98, mode="fused")
+if os.environ.get("TB_PDL") is not None:  # programmatic dependent launch on / off (default: library default)
+    g.temporal(True, pdl=bool(int(os.environ["TB_PDL"])))
 fields = lbgen.rt_macro(LX, LY, 1.0)
 g.init_macro(*fields)
 host.numpy()[:] = g.peek(0).reshape(-1)
