@@ -357,8 +357,8 @@ int lb_sync(lb_ctx* ctx);
  * time-aligned (every strip's main region cut into the same column ranges, the
  * CTAs left over share the remaining columns of every strip: the tail); the
  * cost of a tail column relative to a main-region one, x16 (0 = the default,
- * measured: 17; 16..64), or 1 = the contiguous split instead (strip-major
- * column ranges).  Work split only: results do not depend on it.
+ * measured: 17 when every strip has >= 2 main-region CTAs, else 16; 16..64),
+ * or 1 = the contiguous split instead (strip-major column ranges).  Work split only: results do not depend on it.
  * LB_OPT_TB_PDL (1 = default, 0 = off): the two-step kernel is launched with
  * programmatic dependent launch, so its CTAs start (and compute their work
  * split) on the SMs the previous launch's CTAs free; each waits for the

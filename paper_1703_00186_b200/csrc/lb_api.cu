@@ -871,8 +871,15 @@ static int tb_wall_weight(const lb_ctx* c) {
 }
 // The kernel's split parameter: wall weight | tail weight << 16 (both x16;
 // tail 0: the contiguous split).
-static int tb_split_weights(const lb_ctx* c) {
-  const int tail = !tb_aligned(c) ? 0 : c->tb_tail_w16 >= 16 ? c->tb_tail_w16 : 17;
+// Default tail weight: 17 when each strip has several main-region CTAs
+// (R >= 2: few tail CTAs, each sweeping several short unaligned segments —
+// 1920x2048: R = 7, tail 17 beats 16 by 4 %), 16 when R = 1 (many tail CTAs
+// on long segments — 8192x8192 and 4096x8192: R = 1, tail 16 beats 17 by
+// 1.9 % / 1.1 %; tools/gpu_job_r02_wt_big.sh).
+static int tb_split_weights(const lb_ctx* c, int G) {
+  const int ns = (c->g.ly + lbk::tb_strip_height() - 1) / lbk::tb_strip_height();
+  const int R = ns > 0 ? G / ns : 0;
+  const int tail = !tb_aligned(c) ? 0 : c->tb_tail_w16 >= 16 ? c->tb_tail_w16 : R >= 2 ? 17 : 16;
   return tb_wall_weight(c) | (tail << 16);
 }
 
@@ -911,7 +918,7 @@ static int step_tb(lb_ctx* c) {
   }
   TRY(launch(c, c->p.collision ? "k_step2_tb_reg" : "k_step2_tb", c->s, 2 * c->L.sites, [&] {
     return lbk::launch_step2_tb(c->g, c->tb, c->par, c->B, c->p.bc_y, c->p.collision, c->relax, grid, c->tb_l2,
-                                tb_split_weights(c), mon, peers ? 1 : 0, inpull ? &pull : nullptr, c->s,
+                                tb_split_weights(c, G), mon, peers ? 1 : 0, inpull ? &pull : nullptr, c->s,
                                 c->tb_pdl != 0 && !peers);  // (peers: ranks sharing a GPU in tests must not
                                                             // park next-launch CTAs on SMs a neighbour needs)
   }));

@@ -462,7 +462,8 @@ class Lattice:
         (0 = the library default: 21 with the time-aligned split; contiguous: 19 BGK, 20 regularised);
         l2_promotion: L2 promotion of its TMA loads in bytes (None = library default);
         tail_weight16: cost of a tail-region column of the time-aligned split,
-        x16 (0 = the library default, 17; 1 = the contiguous split instead);
+        x16 (0 = the library default: 17 with >= 2 main-region CTAs per strip, else 16;
+        1 = the contiguous split instead);
         pdl: programmatic dependent launch of the kernel (None = library default, on)."""
         _check(lib().lb_set_option(self._ctx, 3, int(enable)))
         _check(lib().lb_set_option(self._ctx, 4, int(grid)))
