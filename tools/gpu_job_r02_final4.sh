@@ -1,7 +1,7 @@
 #!/bin/bash
 # round 2 final evidence on the aligned-split + PDL kernel: GPU tests, smoke, bench lines (K = 1000 default, the
 # driver's K = 20, configs #3 / #4), reference arm, ncu launch list, ncu metrics, --set full of k_step2_tb
-O=gpurun_out/r02final4
+O=${O:-gpurun_out/r02final4}
 mkdir -p $O
 timeout 1500 python -m pytest tests -m gpu -q > $O/gpu_tests.log 2>&1; tail -1 $O/gpu_tests.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; tail -1 $O/smoke.log

@@ -28,7 +28,7 @@ def main():
     fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
     res = {"lx": lx, "ly": ly, "launches": []}
     for coll in ("bgk", "regularized"):
-        g = lbm.Lattice(lx, ly, collision=coll, temporal=True)
+        g = lbm.Lattice(lx, ly, collision=coll, temporal=True, bc_y=os.environ.get("TB_BC", "thermal"))
         if os.environ.get("TB_WW") or os.environ.get("TB_TW"):  # wall-strip / tail weights x16 (work split)
             g.temporal(True, wall_weight16=int(os.environ.get("TB_WW", "0")),
                        tail_weight16=int(os.environ.get("TB_TW", "0")))
