@@ -71,15 +71,15 @@
 // clusters of 2 CTAs sweeping adjacent strips in lockstep (see the kernel;
 // variant builds only: -3 %, the per-iteration cluster barrier costs more than
 // the 208-row store runs gain)
+#ifndef LB_TB_PAIR
+#define LB_TB_PAIR 0
+#endif
 // phase-2 warp rotation (see the kernel; 0 = warp NW1 + k handles row block k).
 // Measured neutral (rotations 0 / 1 / 2 at the tuned weights: 17.85K / 17.79K /
 // 17.83K, then 17.65K / 17.81K / 17.77K): the wall strips' extra cost is not
 // scheduler contention.  Variant builds only.
 #ifndef LB_TB_P2ROT
 #define LB_TB_P2ROT 0
-#endif
-#ifndef LB_TB_PAIR
-#define LB_TB_PAIR 0
 #endif
 #ifndef LB_TB_CLOCK  // variant builds only: per-CTA start/end times (tools/tb_clock.py)
 #define LB_TB_CLOCK 0
@@ -796,8 +796,9 @@ __global__ void __launch_bounds__(TbCfg<HT, PF>::NT, 1)
   const uint32_t bar_cp = smem_u32(bars + NB + 4);  // TMEM: copies of phase-1 item k done: bar_cp + 8 (k & 1)
   // TMEM: this phase-2 warp's lane quarter
   const uint32_t tlane = tbase + ((uint32_t)(32 * (warp & 3)) << 16);
-  // phase-2 warp w handles the strip rows of block (w - NW1 + P2ROT) mod NW2:
-  // rotated so that the warps holding the wall band rows of the two phases
+  // phase-2 warp w handles the strip rows of block (w - NW1 + P2ROT) mod NW2
+  // (variant builds; P2ROT = 0 by default): rotation would place the warps
+  // holding the wall band rows of the two phases
   // (the thermal repopulation and the virtual-row copies) sit on different
   // schedulers (warp w issues on scheduler w mod 4: unrotated, phase 1's
   // rows [ya-3, ya+29) and phase 2's [ya, ya+32) both land on scheduler 0 at
