@@ -508,6 +508,15 @@ def main():
             g.gather(out=host_out.numpy() if host_out is not None else None)   # synchronising
         e2e_s = max_over_ranks(time.perf_counter() - t)
         m = mon.numpy()
+        if world > 1:
+            # (after the timed region) the per-step results are this rank's
+            # slab (lb_invariants_pair_async is not collective): sum over ranks
+            dev = "cpu" if same_gpu else "cuda"
+            sums = torch.from_numpy(m[:, :4].copy()).to(dev)
+            mins = torch.from_numpy(m[:, 4].copy()).to(dev)
+            dist.all_reduce(sums, op=dist.ReduceOp.SUM)
+            dist.all_reduce(mins, op=dist.ReduceOp.MIN)
+            m = np.concatenate([sums.cpu().numpy(), mins.cpu().numpy()[:, None]], axis=1)
         mass_drift = float(abs(m[-1, 0] - m[0, 0]) / m[0, 0])
         line["e2e"] = {"value": round(sites_all * k_e2e / e2e_s / 1e6, 2), "unit": "MLUPS",
                        "h2d_bytes_per_step": state_bytes / k_e2e,

@@ -313,7 +313,9 @@ int lb_invariants_async(lb_ctx* ctx, double* host_out);
  * two-step kernel wrote (so a two-step lb_step(2) still yields one result per
  * time step).  host_out: 10 doubles, page-locked for true asynchrony; valid
  * after the next lb_sync.  LB_ESTATE if the last step was not such a launch.
- * Non-physical results set the sticky flag lb_sync reports (as above). */
+ * Non-physical results set the sticky flag lb_sync reports (as above).  Not
+ * collective: at N > 1 the values are this rank's slab (sum them over ranks,
+ * e.g. after the run; lb_invariants is the collective form). */
 int lb_invariants_pair_async(lb_ctx* ctx, double* host_out);
 
 /* Waits for the context's streams.  LB_EPEER if a peer wait timed out;
