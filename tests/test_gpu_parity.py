@@ -774,6 +774,49 @@ def test_two_step_kernel_l2_promotion(lb):
 
 
 @pytest.mark.parametrize("coll", ["bgk", "regularized"])
+@pytest.mark.parametrize("lx,ly,grid", [(240, 520, 0), (96, 1040, 0), (48, 7800, 0), (200, 214, 37), (64, 104, 0)])
+def test_two_step_work_split_and_pdl(lb, coll, lx, ly, grid):
+    """The time-aligned work split (default), its tail / wall weights, the
+    contiguous split (LB_OPT_TB_TAIL_WEIGHT = 1) and programmatic dependent
+    launch on / off only change which CTA sweeps which columns and when a
+    launch may start: every combination gives the one-step kernel's bits, with
+    monitors on the per-step invariants agree to rounding, and illegal values
+    are rejected.  Shapes (148 CTAs unless given): R = 29 / 14 main ranges per
+    strip and a tail of 3 / 8 CTAs, R = 1 (75 strips, 73 tail CTAs), an odd CTA
+    count (37 CTAs on 3 strips), one strip (no aligned split)."""
+    st = oracle_state(lx, ly, seed=lx + ly)
+    ref = lb.Lattice(lx, ly, collision=coll, temporal=False)
+    ref.set_state(st)
+    ref.step(6)
+    want = ref.gather()
+    ref.close()
+    invs = []
+    for tail, wall, pdl in ((0, 0, True), (1, 0, True), (16, 24, False), (40, 17, True), (17, 21, False)):
+        g = lb.Lattice(lx, ly, collision=coll)
+        g.temporal(True, grid=grid, tail_weight16=tail, wall_weight16=wall, pdl=pdl)
+        g.monitor(True)
+        g.set_state(st)
+        out = np.zeros(10)
+        for _ in range(3):
+            g.step(2)
+            g.invariants_pair_async(out)
+        g.sync()
+        invs.append(out.copy())
+        assert np.array_equal(g.gather(), want), (tail, wall, pdl)
+        for bad in ((lambda: g.temporal(True, tail_weight16=8)), (lambda: g.temporal(True, tail_weight16=65)),
+                    (lambda: lb.lib().lb_set_option(g._ctx, 10, 2))):
+            r = None
+            try:
+                r = bad()
+            except lb.LBError:
+                r = "raised"
+            assert r == "raised" or r != 0
+        g.close()
+    for v in invs[1:]:
+        assert np.allclose(v, invs[0], rtol=1e-13, atol=1e-13 * abs(invs[0][0]))
+
+
+@pytest.mark.parametrize("coll", ["bgk", "regularized"])
 @pytest.mark.parametrize("grid,l2", [(1, 0), (7, 4), (300, 8)])
 def test_two_step_kernel_grid_and_prefetch(lb, grid, l2, coll):
     """Any CTA count (one CTA sweeping everything, uneven ranges, more CTAs than
