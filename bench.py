@@ -58,10 +58,11 @@ class ClockSampler:
         0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
     }
 
-    def __init__(self, index: int, period: float = 0.001):
+    def __init__(self, index: int, period: float = 0.0002):
         self.samples, self.reasons, self.max_mhz = [], set(), None
         self.period = period
         self._stop = threading.Event()
+        self._active = threading.Event()   # samples count only between begin() and end()
         self._t = None
         try:
             import pynvml
@@ -75,15 +76,26 @@ class ClockSampler:
     def _run(self):
         nv = self.nv
         while not self._stop.is_set():
+            if not self._active.is_set():
+                self._active.wait(0.01)
+                continue
             try:
-                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                mhz = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)   # ~0.4 ms per query
                 r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                for bit, name in self.REASONS.items():
-                    if r & bit and bit != 0x1:
-                        self.reasons.add(name)
+                if self._active.is_set():
+                    self.samples.append(mhz)
+                    for bit, name in self.REASONS.items():
+                        if r & bit and bit != 0x1:
+                            self.reasons.add(name)
             except Exception:
                 pass
             time.sleep(self.period)
+
+    def begin(self):
+        self._active.set()
+
+    def end(self):
+        self._active.clear()
 
     def __enter__(self):
         if self.nv is not None:
@@ -92,6 +104,7 @@ class ClockSampler:
         return self
 
     def __exit__(self, *a):
+        self._active.clear()
         self._stop.set()
         if self._t is not None:
             self._t.join()
@@ -352,12 +365,15 @@ def main():
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(dev_index) as clk:
+    with ClockSampler(dev_index) as clk:   # thread started before the region, samples counted within it
+        time.sleep(0.005)
+        clk.begin()
         e0.record(stream)
         g.step(args.steps)
         e1.record(stream)
         g.sync()
         torch.cuda.synchronize()
+        clk.end()
     barrier()
     launches = g.launch_count() - launches0
     ms = max_over_ranks(e0.elapsed_time(e1))
