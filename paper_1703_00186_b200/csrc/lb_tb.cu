@@ -78,6 +78,13 @@
 // Measured neutral (rotations 0 / 1 / 2 at the tuned weights: 17.85K / 17.79K /
 // 17.83K, then 17.65K / 17.81K / 17.77K): the wall strips' extra cost is not
 // scheduler contention.  Variant builds only.
+// phase 2 stores only the rows its strip owns (see phase2_update; variant
+// builds only): measured -0.8 % (18.27K vs 18.42K MLUPS, 3 alternating reps) —
+// the 32 overlap rows no longer stored twice, but the top strip's first owned
+// row starts mid-line, so both strips write partial 128-byte lines
+#ifndef LB_TB_STORE_OWNED
+#define LB_TB_STORE_OWNED 0
+#endif
 #ifndef LB_TB_P2ROT
 #define LB_TB_P2ROT 0
 #endif
@@ -536,6 +543,11 @@ __device__ __forceinline__ void phase2_update(double (&f)[Q], double* __restrict
     else if (MON && own) acc_invariants(m, r, acc);
   };
   tb_collide<COLL>(f, r, hook);
+  // LB_TB_STORE_OWNED: only the rows this strip owns are stored — the top
+  // strip, moved down to end on the wall, overlaps the strip below by
+  // (nstrips HT - ly) rows (32 at ly = 2048), whose identical values that strip
+  // stores already
+  if (LB_TB_STORE_OWNED && !own) return;
   // 64-bit stride: one IMAD.WIDE per store instead of IMAD + LEA + LEA.HI.X
   const int64_t nyp = opaque(g.nyp);
   double* p = B + (int64_t)c2 * g.cs + g.y0 + y;
