@@ -419,8 +419,9 @@ def main():
     if not hbm_peak:
         hbm_peak, peak_src = 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
     ncu = load_json(os.path.join(ROOT, "profiles", "ncu_summary.json"), {}) or {}
-    fp64 = load_json(os.path.join(ROOT, "profiles", "r01_fp64_hbm_microbench.json"), {}) or {}
-    fp64_peak = fp64.get("fp64_tflops")
+    fp64 = (load_json(os.path.join(ROOT, "profiles", "r02_fp64_hbm_microbench.json"), {})
+            or load_json(os.path.join(ROOT, "profiles", "r01_fp64_hbm_microbench.json"), {}) or {})
+    fp64_peak = fp64.get("fp64_tflops")   # measured DFMA peak (tools/fp64_bench.py, NVML-sampled clock)
 
     # dominant kernel: the two-step kernel k_step2_tb (the default N = 1 path),
     # else every launch of k_step_fused (whole lattice, or bulk + border
@@ -468,6 +469,13 @@ def main():
                                  f"of the same {args.steps} steps"),
                     "peak_source": peak_src,
                     "traffic_source": ncu.get("source") if traffic else None}
+        fl = kn.get("flops_per_site")   # ncu FP64 flops per site per launch (FMA = 2)
+        if fl and fp64_peak:
+            # the collisions' FP64 rate inside the dominant kernel (BASELINE's "collide
+            # FP64 % of peak"): not its bound, reported beside the HBM roofline
+            tf = fl * sites_per_launch / (avg_ms * 1e-3) / 1e12
+            roofline["fp64"] = {"flops_per_site_per_launch": fl, "tflops": round(tf, 2),
+                                "peak_tflops": fp64_peak, "frac": round(tf / fp64_peak, 4)}
         if two_step:
             roofline["steps_per_launch"] = 2
             roofline["one_step_equivalent_gbs"] = round(2 * achieved, 1)
